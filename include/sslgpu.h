@@ -1,0 +1,174 @@
+/*
+ * sslgpu.h — C ABI of the B200-native GSVD-MUSIC sound-source-localization
+ * engine (libsslgpu.so).
+ *
+ * This is the drop-in boundary for the reference's localization hot path.
+ * The reference (sslkit, /root/reference/proj) exposes that path only as a
+ * C++ API over STL value types in namespace ssl; every entry point below
+ * replaces one of those calls with plain pointers, sizes and an int status,
+ * so any FFI (ctypes, cgo, JNI, N-API) or the C++ shim in
+ * include/sslgpu/ssl.hpp can bind it.  Reference interfaces are cited as
+ * include/ssl/<file>:<line> relative to /root/reference/proj.
+ *
+ * Tensor layouts are the reference's own (interleaved complex, row-major):
+ *   spectrum frame  X  [m][bins]        cf32  (SpectrumFrame::spectra[m][b], types.hpp:56-61)
+ *   correlation     R  [bins][m][m]     cf32  (CorrelationSet::bins[b], correlation.hpp:14-21)
+ *   noise model     K  [bins][m][m]     cf32  (NoiseModel::k, gsvd.hpp:31-50)
+ *   steering        H  [dirs][bins][m]  cf32  (SteeringField::vectors, music.hpp:32-47)
+ *   left factors    E  [bins][m][m]     cf64  row-major, column j = vector j
+ *                                             (GsvdBinResult::e, gsvd.hpp:52-60)
+ *   power           P  [dirs] f64, bin power [bins][dirs] f64 (MusicSpectrum, music.hpp:66-71)
+ *
+ * Status codes mirror the reference's error taxonomy (types.hpp:13-23) and
+ * its CLI exit codes (tools/sslkit.cpp:280-291).  There is no CPU fallback:
+ * every compute entry point runs on the GPU and fails with SSLG_DEVICE if no
+ * device is usable.
+ *
+ * Contexts are not thread-safe (one per stream, like CorrelationWindow,
+ * SPEC.md:124); many contexts may share one device.
+ */
+#ifndef SSLGPU_H
+#define SSLGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSLG_OK 0
+#define SSLG_VALIDATION 2 /* ssl::ValidationError */
+#define SSLG_NUMERICAL 3  /* ssl::NumericalError */
+#define SSLG_IO 4         /* ssl::IoError */
+#define SSLG_DEVICE 5     /* CUDA failure / no device */
+
+#define SSLG_MAX_M 64 /* channels handled by the SMEM-resident solver */
+
+typedef struct sslg_ctx sslg_ctx;
+
+/* Engine configuration.  Solver / music fields mirror ssl::SolverConfig
+ * (gsvd.hpp:14-26) and ssl::MusicConfig (music.hpp:49-62). */
+typedef struct sslg_config {
+    uint32_t m;                  /* channels (<= SSLG_MAX_M) */
+    uint32_t bins;               /* retained STFT bins (StftConfig::bin_count) */
+    uint32_t dirs;               /* direction-grid size; 0 until set_steering */
+    uint32_t window_frames;      /* T of CorrelationWindow (correlation.hpp:29-31) */
+    uint32_t rebuild_interval;   /* CorrelationWindow rebuild cadence, default 1000 */
+    uint32_t num_sources;        /* MusicConfig::num_sources */
+    float denominator_floor;     /* MusicConfig::denominator_floor, default 1e-12 */
+    int squared_denominator;     /* MusicConfig::squared_denominator */
+    float low_power_ratio;       /* MusicConfig::low_power_ratio, default 1.25 */
+    int pivoting;                /* SolverConfig::pivoting: 0 none, 1 partial */
+    int canonical_subspaces;     /* SolverConfig::canonical_subspaces */
+    int refine_leading;          /* A A^H sharpening of the kept span (gsvd.cpp:440-466), default 1 */
+    uint32_t max_sweeps;         /* Jacobi sweep cap, 0 = 60 (jacobi_svd, gsvd.cpp:631) */
+    uint32_t max_batch;          /* blocks (frames) processed per launch; sizes device buffers */
+    int device;                  /* CUDA device ordinal */
+    void* stream;                /* cudaStream_t to launch on; NULL = the context's own stream */
+} sslg_config;
+
+/* Fills `cfg` with the reference defaults (gsvd.hpp:14-26, music.hpp:49-62,
+ * pipeline.hpp:23, correlation.hpp:31). */
+void sslg_config_default(sslg_config* cfg);
+
+int sslg_create(sslg_ctx** out, const sslg_config* cfg);
+void sslg_destroy(sslg_ctx* ctx);
+/* Message of the last failure on this thread (any context). */
+const char* sslg_last_error(void);
+/* Reads back the effective configuration. */
+int sslg_get_config(const sslg_ctx* ctx, sslg_config* cfg);
+
+/* ---- setup ------------------------------------------------------------ */
+
+/* NoiseModel: uploads K, builds K^-1 on the device with the float and double
+ * Gauss-Jordan of mat_inverse<T> (gsvd.cpp:21-62, prepare_inverses 756-768);
+ * with check_pd also runs check_positive_definite (gsvd.cpp:736-754).
+ * Failures return SSLG_NUMERICAL and set *bad_bin (nullable) to the first
+ * offending bin, like the reference's "... at bin b" messages. */
+int sslg_set_noise_model(sslg_ctx* ctx, const float* k, int check_pd, uint32_t* bad_bin);
+/* NoiseModel::identity (gsvd.cpp:722-727). */
+int sslg_set_noise_identity(sslg_ctx* ctx);
+
+/* SteeringField + DirectionTopology: h [dirs][bins][m] cf32, dirs_deg
+ * [dirs][2] (azimuth, elevation), and the neighbor lists of
+ * DirectionTopology::build (music.cpp:176-195) as CSR (nbr_off [dirs+1],
+ * nbr [nbr_off[dirs]]).  Pass nbr_off == NULL to build the topology here
+ * with sslg_build_topology(radius_deg = 10, pipeline.cpp:222). */
+int sslg_set_steering(sslg_ctx* ctx, uint32_t dirs, const float* h, const double* dirs_deg,
+                      const uint32_t* nbr_off, const uint32_t* nbr);
+
+/* DirectionTopology::build (music.cpp:176-195) on the host, same FP64 test
+ * dot >= cos(radius): writes nbr_off [n+1] and up to `cap` neighbors.
+ * Returns SSLG_VALIDATION (and the needed size in *nnz) if cap is short. */
+int sslg_build_topology(const double* dirs_deg, uint32_t n, double radius_deg, uint32_t* nbr_off, uint32_t* nbr,
+                        uint32_t cap, uint32_t* nnz);
+
+/* ---- streaming hot path (run_locate's per-frame loop, pipeline.cpp:227-245) */
+
+/* Estimates of one emitted block.  Mirrors FrameEstimates + SourceEstimate
+ * (pipeline.hpp:63-66, music.hpp:88-93); arrays hold num_sources slots. */
+typedef struct sslg_block_out {
+    uint32_t frame_index; /* frame that completed the block */
+    uint32_t count;       /* estimates written (<= num_sources) */
+} sslg_block_out;
+
+/* Pushes `nframes` spectrum frames x [nframes][m][bins] cf32 (host memory)
+ * through the correlation window; for every frame that leaves the window
+ * full runs GSVD -> MUSIC -> integration -> peak search on the device and
+ * writes one block of results: blocks[e], est_idx / est_power / est_low
+ * [e][num_sources], and (nullable) power [e][dirs].  *emitted receives the
+ * block count (nframes minus the frames still filling the window). */
+int sslg_push_frames(sslg_ctx* ctx, const float* x, uint32_t nframes, sslg_block_out* blocks, uint32_t* est_idx,
+                     double* est_power, uint8_t* est_low, double* power, uint32_t* emitted);
+
+/* Same on device-resident frames (x_dev: device pointer, same layout);
+ * results stay on the device until sslg_read_results.  Asynchronous on the
+ * context stream. */
+int sslg_push_frames_device(sslg_ctx* ctx, const void* x_dev, uint32_t nframes, uint32_t* emitted);
+/* Copies the results of the last push (blocks [0, n)) to host arrays
+ * (any may be NULL). */
+int sslg_read_results(sslg_ctx* ctx, uint32_t n, sslg_block_out* blocks, uint32_t* est_idx, double* est_power,
+                      uint8_t* est_low, double* power, double* bin_power, double* sigma, uint32_t* sweeps,
+                      uint8_t* conv);
+/* Clears the correlation window (a fresh CorrelationWindow). */
+int sslg_reset_window(sslg_ctx* ctx);
+/* Blocks until the context stream is idle. */
+int sslg_synchronize(sslg_ctx* ctx);
+
+/* ---- stage entry points (host buffers, one call per reference function) */
+
+/* CorrelationWindow push + normalized (correlation.cpp:86-130) for nframes
+ * frames; r_out [emitted][bins][m][m] cf32 bit-identical to the reference. */
+int sslg_correlation(sslg_ctx* ctx, const float* x, uint32_t nframes, float* r_out, uint32_t* emitted);
+
+/* gsvd / gsvd_reference batch drivers (gsvd.hpp:160-163) for nsets
+ * correlation sets r [nsets][bins][m][m]: sigma [nsets][bins][m] descending,
+ * e [nsets][bins][m][m] (row-major, column j = vector j), sweeps / conv
+ * [nsets][bins] (nullable).  FP64 one-sided Jacobi + canonicalization. */
+int sslg_gsvd(sslg_ctx* ctx, const float* r, uint32_t nsets, double* sigma, double* e, uint32_t* sweeps,
+              uint8_t* conv);
+
+/* calc_average_power (music.cpp:112-165) on left factors e [nsets][bins][m][m]
+ * (as returned by sslg_gsvd): power [nsets][dirs], bin_power
+ * [nsets][bins][dirs] (nullable). */
+int sslg_spectrum(sslg_ctx* ctx, const double* e, uint32_t nsets, double* power, double* bin_power);
+
+/* peak_search (music.cpp:197-236) on power [nsets][dirs] with the context's
+ * topology: est_* [nsets][num_sources], count [nsets]. */
+int sslg_peaks(sslg_ctx* ctx, const double* power, uint32_t nsets, uint32_t* est_idx, double* est_power,
+               uint8_t* est_low, uint32_t* count);
+
+/* ---- measurement ---------------------------------------------------------- */
+
+/* Device time (ms) of each stage of the last push, measured with CUDA events
+ * on the context stream: [0] correlation, [1] jacobi, [2] canonical,
+ * [3] spectrum, [4] peaks. */
+int sslg_last_stage_ms(const sslg_ctx* ctx, float* ms5);
+/* Number of kernel launches issued by the last push / stage call. */
+uint32_t sslg_last_launch_count(const sslg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSLGPU_H */

@@ -1,0 +1,81 @@
+// Shared device helpers for the sm_100a GSVD-MUSIC kernels.
+//
+// Complex values are interleaved (re, im) pairs: float2 for the FP32 tensors
+// the reference stores (spectra, R, K, steering: include/ssl/types.hpp:25-26,
+// correlation.hpp:14-21, music.hpp:32-47) and double2 for everything the
+// solver computes (A, W, E, P), so every stored tensor keeps the reference's
+// memory layout and only the arithmetic precision is chosen here.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sslg {
+
+constexpr int kMaxM = 64;       // channels handled by the SMEM-resident solver
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// conj(a) * b
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double2 f2d(float2 a) { return make_double2((double)a.x, (double)a.y); }
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m, unsigned mask = 0xffffffffu) {
+    return __shfl_xor_sync(mask, v, m);
+}
+
+// Lanes of the aligned W-lane group that contains this thread.  Reductions
+// over a group name only that group, so groups may diverge independently.
+template <int W>
+__device__ __forceinline__ unsigned group_mask() {
+    if (W >= 32) return 0xffffffffu;
+    return ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
+}
+
+template <int W>
+__device__ __forceinline__ double group_sum(double v) {
+    const unsigned mask = group_mask<W>();
+#pragma unroll
+    for (int m = W / 2; m > 0; m >>= 1) v += __shfl_xor_sync(mask, v, m);
+    return v;
+}
+
+template <int W>
+__device__ __forceinline__ double2 group_sum2(double2 v) {
+    const unsigned mask = group_mask<W>();
+#pragma unroll
+    for (int m = W / 2; m > 0; m >>= 1) {
+        v.x += __shfl_xor_sync(mask, v.x, m);
+        v.y += __shfl_xor_sync(mask, v.y, m);
+    }
+    return v;
+}
+
+// block-wide helpers -------------------------------------------------------
+
+// Round-robin (circle method) pairing for an even number of columns n:
+// round r in [0, n-1), pair g in [0, n/2).  Every unordered pair appears
+// exactly once per sweep and each column once per round.
+__device__ __forceinline__ void rr_pair(int r, int g, int n, int& p, int& q) {
+    int a, b;
+    if (g == 0) {
+        a = n - 1;
+        b = r;
+    } else {
+        a = (r + g) % (n - 1);
+        b = (r - g + (n - 1)) % (n - 1);
+    }
+    p = a < b ? a : b;
+    q = a < b ? b : a;
+}
+
+}  // namespace sslg

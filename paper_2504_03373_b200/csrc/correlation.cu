@@ -1,0 +1,138 @@
+// Kernel (1): sliding-window spatial correlation R(w) = (1/T) sum X X^H.
+//
+// Follows CorrelationWindow (reference proj/src/correlation.cpp:53-130):
+// an FP64 running sum over the full M x M matrix, updated per push by
+// subtracting the frame leaving the window and adding the new one
+// (correlation.cpp:103-106), rebuilt oldest-first every `rebuild_interval`
+// pushes (75-84), and normalized as float(sum * (1/T)) (112-130).
+//
+// Bit-exactness: X entries are float, so every product of two entries is
+// exact in double; the only roundings are (a*c + b*d), the running-sum add and
+// the final scale/narrow.  They are issued with explicit _rn intrinsics so the
+// compiler cannot contract them differently, which makes R bit-identical to
+// the reference's for the same push sequence.
+//
+// Layout: one CTA per frequency bin; each thread owns up to kPer entries of
+// that bin's M x M running sum in registers for the whole launch, so the FP64
+// state is read and written once per launch however many frames it ingests.
+// The frames of a launch are consumed in order (the recurrence is sequential
+// in time); parallelism is over bins x matrix entries.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sslg {
+
+constexpr int kCorrThreads = 512;
+constexpr int kCorrPer = (kMaxM * kMaxM + kCorrThreads - 1) / kCorrThreads;  // 8
+
+__device__ __forceinline__ void outer_acc(double2& acc, float2 xi, float2 xj, bool subtract) {
+    const double a = xi.x, b = xi.y, c = xj.x, d = xj.y;
+    // xi * conj(xj): (a*c + b*d, b*c - a*d), one rounding each (products exact)
+    const double re = __fma_rn(a, c, __dmul_rn(b, d));
+    const double im = __fma_rn(b, c, -__dmul_rn(a, d));
+    if (subtract) {
+        acc.x = __dadd_rn(acc.x, -re);
+        acc.y = __dadd_rn(acc.y, -im);
+    } else {
+        acc.x = __dadd_rn(acc.x, re);
+        acc.y = __dadd_rn(acc.y, im);
+    }
+}
+
+__global__ void __launch_bounds__(kCorrThreads) correlation_kernel(CorrArgs a) {
+    __shared__ float2 xs_new[kMaxM];
+    __shared__ float2 xs_old[kMaxM];
+    const int b = blockIdx.x;
+    const int m = a.m;
+    const int mm = m * m;
+    const int tid = threadIdx.x;
+
+    double2 acc[kCorrPer];
+    int ei[kCorrPer], ej[kCorrPer];
+#pragma unroll
+    for (int k = 0; k < kCorrPer; ++k) {
+        const int e = tid + k * kCorrThreads;
+        ei[k] = e / m;
+        ej[k] = e % m;
+        acc[k] = e < mm ? a.state[(size_t)b * mm + e] : make_double2(0, 0);
+    }
+    const double inv_t = 1.0 / (double)a.t;
+    long long pushed = a.pushed0;
+    long long since = a.since0;
+    long long first_emit = (long long)a.t - 1 - a.pushed0;
+    if (first_emit < 0) first_emit = 0;
+
+    auto frame_ptr = [&](long long g) { return a.ring + (size_t)(g % a.cap) * m * a.bins; };
+
+    for (int f = 0; f < a.frames; ++f) {
+        const long long g = a.pushed0 + f;
+        const bool drop_old = pushed >= a.t;
+        __syncthreads();
+        if (tid < m) xs_new[tid] = frame_ptr(g)[(size_t)tid * a.bins + b];
+        else if (drop_old && tid < 2 * m) xs_old[tid - m] = frame_ptr(g - a.t)[(size_t)(tid - m) * a.bins + b];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kCorrPer; ++k) {
+            if (tid + k * kCorrThreads < mm) {
+                if (drop_old) outer_acc(acc[k], xs_old[ei[k]], xs_old[ej[k]], true);
+                outer_acc(acc[k], xs_new[ei[k]], xs_new[ej[k]], false);
+            }
+        }
+        ++pushed;
+        if (++since >= a.rebuild_interval) {
+            // rebuild oldest first (correlation.cpp:75-84)
+            const long long have = pushed < a.t ? pushed : a.t;
+#pragma unroll
+            for (int k = 0; k < kCorrPer; ++k) acc[k] = make_double2(0, 0);
+            for (long long kk = 0; kk < have; ++kk) {
+                const long long gg = pushed - have + kk;
+                __syncthreads();
+                if (tid < m) xs_new[tid] = frame_ptr(gg)[(size_t)tid * a.bins + b];
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < kCorrPer; ++k)
+                    if (tid + k * kCorrThreads < mm) outer_acc(acc[k], xs_new[ei[k]], xs_new[ej[k]], false);
+            }
+            since = 0;
+        }
+        if (f >= first_emit) {
+            float2* r = a.r_out + ((size_t)(f - first_emit) * a.bins + b) * mm;
+#pragma unroll
+            for (int k = 0; k < kCorrPer; ++k) {
+                const int e = tid + k * kCorrThreads;
+                if (e < mm)
+                    r[e] = make_float2(__double2float_rn(__dmul_rn(acc[k].x, inv_t)),
+                                       __double2float_rn(__dmul_rn(acc[k].y, inv_t)));
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kCorrPer; ++k) {
+        const int e = tid + k * kCorrThreads;
+        if (e < mm) a.state[(size_t)b * mm + e] = acc[k];
+    }
+}
+
+// Non-finite guard (correlation.cpp:90-95): counts non-finite spectrum values
+// of the frames about to be ingested.
+__global__ void count_nonfinite_kernel(const float* p, size_t n, unsigned int* bad) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    unsigned int local = 0;
+    for (; i < n; i += stride) local += isfinite(p[i]) ? 0u : 1u;
+    if (local) atomicAdd(bad, local);
+}
+
+void launch_correlation(const CorrArgs& a, cudaStream_t s) {
+    correlation_kernel<<<a.bins, kCorrThreads, 0, s>>>(a);
+}
+
+void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStream_t s) {
+    const int threads = 256;
+    size_t blocks = (n + threads - 1) / threads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) blocks = 1;
+    count_nonfinite_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, n, bad);
+}
+
+}  // namespace sslg

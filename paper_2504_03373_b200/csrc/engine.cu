@@ -1,0 +1,733 @@
+// Host engine behind the C ABI of include/sslgpu.h.
+//
+// Owns the device-resident state of one localization stream: the noise model
+// (K and the FP64 K^-1), the transposed steering table with |h|^2, the
+// topology CSR, the spectrum-frame ring and FP64 running correlation sum, and
+// the per-block work buffers (R, sigma, E, P, Pbar, estimates).  A push of F
+// frames is one pass over the hot path:
+//
+//   ring <- frames (H2D or D2D)      non-finite gate
+//   correlation_kernel   grid bins                      -> R  [F'][bins][m][m]
+//   jacobi_kernel        grid F' x bins                 -> sigma, E (sorted)
+//   canonical_kernel     grid F' x bins                 -> E canonicalized
+//   spectrum_kernel      grid F' x bins x dir-chunks    -> P  [F'][bins][dirs]
+//   integrate_peaks      grid F'                        -> Pbar, estimates
+//
+// where F' = frames that complete a full window.  Everything runs on one CUDA
+// stream (the caller's, if given) with CUDA events between stages; nothing on
+// the path falls back to the CPU.
+#include "../../include/sslgpu.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace sslg {
+
+// [n][m][m] transpose of the trailing square (row-major <-> vector-major)
+__global__ void transpose_sq_kernel(const double2* __restrict__ in, double2* __restrict__ out, int m, size_t n) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t mm = (size_t)m * m;
+    if (idx >= n * mm) return;
+    const size_t b = idx / mm;
+    const int e = (int)(idx % mm);
+    const int i = e / m, j = e % m;
+    out[b * mm + (size_t)j * m + i] = in[idx];
+}
+
+}  // namespace sslg
+
+using namespace sslg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return set_err(SSLG_DEVICE, std::string(#call ": ") + cudaGetErrorString(e_));         \
+    } while (0)
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) return 0;
+    CU(cudaMalloc((void**)p, n * sizeof(T)));
+    return 0;
+}
+
+}  // namespace
+
+struct sslg_ctx {
+    sslg_config cfg{};
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // noise model
+    float2* k = nullptr;
+    double2* kinv = nullptr;
+    bool have_noise = false;
+    // steering
+    uint32_t dirs = 0;
+    float2* h_raw = nullptr;  // [dirs][bins][m] staging
+    float2* h_t = nullptr;    // [bins][dirs][m]
+    double* num = nullptr;    // [bins][dirs]
+    uint32_t* nbr_off = nullptr;
+    uint32_t* nbr = nullptr;
+    uint32_t nnz = 0;
+    bool have_steering = false;
+    // window
+    float2* ring = nullptr;
+    int cap = 0;
+    double2* state = nullptr;
+    long long pushed = 0;
+    long long since = 0;
+    // work buffers (max_batch blocks)
+    float2* r = nullptr;
+    double* sigma = nullptr;
+    double2* e = nullptr;
+    double2* e_tmp = nullptr;
+    uint32_t* sweeps = nullptr;
+    uint8_t* conv = nullptr;
+    double* p = nullptr;
+    double* power = nullptr;
+    uint32_t* est_idx = nullptr;
+    double* est_pw = nullptr;
+    uint8_t* est_low = nullptr;
+    uint32_t* est_count = nullptr;
+    unsigned int* flags = nullptr;  // [0] nonfinite, [1] bad_f, [2] bad_d, [3] herm, [4] pd
+    // last push bookkeeping
+    uint32_t last_emitted = 0;
+    long long last_first_frame = 0;
+    uint32_t launches = 0;
+    cudaEvent_t ev[6] = {};
+    bool timed = false;
+};
+
+namespace {
+
+int sync_flags(sslg_ctx* c, unsigned int* host, int n) {
+    CU(cudaMemcpyAsync(host, c->flags, n * sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    return 0;
+}
+
+int reset_flags(sslg_ctx* c) {
+    unsigned int init[8] = {0, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0, 0, 0};
+    CU(cudaMemcpyAsync(c->flags, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    return 0;
+}
+
+// SSLG_SYNC_DEBUG=1 synchronizes after every launch so a fault is reported
+// against the kernel that caused it.
+bool sync_debug() {
+    static const bool on = [] {
+        const char* v = std::getenv("SSLG_SYNC_DEBUG");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+
+int check_last_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && sync_debug()) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return set_err(SSLG_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    return 0;
+}
+
+#define TRY(x)                 \
+    do {                       \
+        int rc_ = (x);         \
+        if (rc_) return rc_;   \
+    } while (0)
+
+// Runs GSVD -> (canonical) on n correlation sets already in c->r.
+int run_gsvd(sslg_ctx* c, int n) {
+    const sslg_config& g = c->cfg;
+    GsvdArgs ga{c->r, c->kinv, c->sigma, c->e, c->sweeps, c->conv, (int)g.m, (int)g.bins,
+                g.max_sweeps ? (int)g.max_sweeps : 60};
+    launch_jacobi(ga, n, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("jacobi_kernel"));
+    CU(cudaEventRecord(c->ev[2], c->stream));
+    if (g.canonical_subspaces) {
+        CanonArgs ca{c->r, c->kinv, c->sigma, c->e, (int)g.m, (int)g.bins, g.refine_leading};
+        launch_canonical(ca, n, c->stream);
+        ++c->launches;
+        TRY(check_last_launch("canonical_kernel"));
+    }
+    CU(cudaEventRecord(c->ev[3], c->stream));
+    return 0;
+}
+
+int run_music(sslg_ctx* c, int n) {
+    const sslg_config& g = c->cfg;
+    SpecArgs sa{c->e, c->h_t, c->num, c->p, (int)g.m, (int)g.bins, (int)c->dirs, (int)g.num_sources, 0, 0,
+                (double)g.denominator_floor, g.squared_denominator};
+    launch_spectrum(sa, n, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("spectrum_kernel"));
+    CU(cudaEventRecord(c->ev[4], c->stream));
+    PeakArgs pa{c->p, c->power, c->nbr_off, c->nbr, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                (int)g.bins, (int)c->dirs, (int)g.num_sources, (double)g.low_power_ratio};
+    launch_peaks(pa, n, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("integrate_peaks_kernel"));
+    CU(cudaEventRecord(c->ev[5], c->stream));
+    return 0;
+}
+
+// copies nframes frames (src: host or device) into the ring after the
+// current push count, then gates on non-finite values
+int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind kind) {
+    const sslg_config& g = c->cfg;
+    const size_t fsz = (size_t)g.m * g.bins;
+    uint32_t done = 0;
+    while (done < nframes) {
+        const int slot = (int)((c->pushed + done) % c->cap);
+        const uint32_t run = std::min<uint32_t>(nframes - done, (uint32_t)(c->cap - slot));
+        CU(cudaMemcpyAsync(c->ring + (size_t)slot * fsz, src + (size_t)done * fsz * 2, run * fsz * sizeof(float2),
+                           kind, c->stream));
+        done += run;
+    }
+    TRY(reset_flags(c));
+    // gate every staged slot (a wrapped range is two spans)
+    done = 0;
+    while (done < nframes) {
+        const int slot = (int)((c->pushed + done) % c->cap);
+        const uint32_t run = std::min<uint32_t>(nframes - done, (uint32_t)(c->cap - slot));
+        launch_count_nonfinite(reinterpret_cast<const float*>(c->ring + (size_t)slot * fsz), run * fsz * 2,
+                               c->flags, c->stream);
+        ++c->launches;
+        done += run;
+    }
+    unsigned int fl[1];
+    TRY(sync_flags(c, fl, 1));
+    if (fl[0]) return set_err(SSLG_VALIDATION, "non-finite spectrum value");
+    return 0;
+}
+
+// one chunk of at most max_batch frames already validated in the ring
+int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
+    const sslg_config& g = c->cfg;
+    const long long first_emit = std::max<long long>(0, (long long)g.window_frames - 1 - c->pushed);
+    const int n = (int)std::max<long long>(0, (long long)nframes - first_emit);
+    CU(cudaEventRecord(c->ev[0], c->stream));
+    CorrArgs ca{c->ring, c->state, c->r, (int)g.m, (int)g.bins, (int)g.window_frames, c->cap, (int)nframes,
+                c->pushed, c->since, (int)(g.rebuild_interval ? g.rebuild_interval : 1)};
+    launch_correlation(ca, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("correlation_kernel"));
+    CU(cudaEventRecord(c->ev[1], c->stream));
+    // host mirror of the push counters (correlation.cpp:103-109)
+    for (uint32_t f = 0; f < nframes; ++f) {
+        ++c->pushed;
+        if (++c->since >= (long long)(g.rebuild_interval ? g.rebuild_interval : 1)) c->since = 0;
+    }
+    c->last_first_frame = c->pushed - n;
+    c->last_emitted = (uint32_t)n;
+    if (n > 0) {
+        TRY(run_gsvd(c, n));
+        TRY(run_music(c, n));
+    } else {
+        for (int i = 2; i < 6; ++i) CU(cudaEventRecord(c->ev[i], c->stream));
+    }
+    c->timed = true;
+    *emitted = (uint32_t)n;
+    return 0;
+}
+
+int require_ready(sslg_ctx* c) {
+    if (!c) return set_err(SSLG_VALIDATION, "null context");
+    if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model not set");
+    if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
+    if (c->cfg.num_sources >= c->cfg.m)
+        return set_err(SSLG_VALIDATION, "num_sources must be smaller than the channel count");
+    CU(cudaSetDevice(c->cfg.device));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+void sslg_config_default(sslg_config* cfg) {
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->window_frames = 50;
+    cfg->rebuild_interval = 1000;
+    cfg->num_sources = 1;
+    cfg->denominator_floor = 1e-12f;
+    cfg->squared_denominator = 0;
+    cfg->low_power_ratio = 1.25f;
+    cfg->pivoting = 1;
+    cfg->canonical_subspaces = 1;
+    cfg->refine_leading = 1;
+    cfg->max_sweeps = 0;
+    cfg->max_batch = 16;
+    cfg->device = 0;
+    cfg->stream = nullptr;
+}
+
+const char* sslg_last_error(void) { return g_err.c_str(); }
+
+int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
+    if (!out || !cfg) return set_err(SSLG_VALIDATION, "null argument");
+    *out = nullptr;
+    const sslg_config& g = *cfg;
+    if (g.m < 1 || g.m > SSLG_MAX_M)
+        return set_err(SSLG_VALIDATION, "channel count must be in [1, " + std::to_string(SSLG_MAX_M) + "]");
+    if (g.bins < 1) return set_err(SSLG_VALIDATION, "correlation set has no bins");
+    if (g.window_frames < 1) return set_err(SSLG_VALIDATION, "correlation window length must be >= 1");
+    if (g.num_sources == 0) return set_err(SSLG_VALIDATION, "num_sources must be at least 1");
+    if (!(g.denominator_floor > 0)) return set_err(SSLG_VALIDATION, "denominator_floor must be positive");
+    if (!(g.low_power_ratio >= 0)) return set_err(SSLG_VALIDATION, "low_power_ratio must be non-negative");
+    if (g.max_batch < 1) return set_err(SSLG_VALIDATION, "max_batch must be >= 1");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_err(SSLG_DEVICE, "no CUDA device available (the engine has no CPU fallback)");
+    if (g.device < 0 || g.device >= ndev) return set_err(SSLG_DEVICE, "device ordinal out of range");
+    CU(cudaSetDevice(g.device));
+    auto* c = new sslg_ctx();
+    c->cfg = g;
+    if (c->cfg.rebuild_interval < 1) c->cfg.rebuild_interval = 1;
+    if (g.stream) {
+        c->stream = static_cast<cudaStream_t>(g.stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete c;
+            return set_err(SSLG_DEVICE, "cudaStreamCreate failed");
+        }
+        c->own_stream = true;
+    }
+    const size_t mm = (size_t)g.m * g.m;
+    const size_t B = g.bins, NB = g.max_batch;
+    c->cap = (int)(g.window_frames + g.max_batch);
+    int rc = 0;
+    rc |= dalloc(&c->k, B * mm);
+    rc |= dalloc(&c->kinv, B * mm);
+    rc |= dalloc(&c->ring, (size_t)c->cap * g.m * B);
+    rc |= dalloc(&c->state, B * mm);
+    rc |= dalloc(&c->r, NB * B * mm);
+    rc |= dalloc(&c->sigma, NB * B * g.m);
+    rc |= dalloc(&c->e, NB * B * mm);
+    rc |= dalloc(&c->e_tmp, NB * B * mm);
+    rc |= dalloc(&c->sweeps, NB * B);
+    rc |= dalloc(&c->conv, NB * B);
+    rc |= dalloc(&c->est_count, NB);
+    rc |= dalloc(&c->flags, 8);
+    for (int i = 0; i < 6 && !rc; ++i)
+        if (cudaEventCreate(&c->ev[i]) != cudaSuccess) rc = set_err(SSLG_DEVICE, "cudaEventCreate failed");
+    if (!rc && cudaMemsetAsync(c->state, 0, B * mm * sizeof(double2), c->stream) != cudaSuccess)
+        rc = set_err(SSLG_DEVICE, "cudaMemset failed");
+    if (rc) {
+        sslg_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return SSLG_OK;
+}
+
+void sslg_destroy(sslg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->k,      c->kinv,  c->h_raw, c->h_t,   c->num,     c->nbr_off, c->nbr,
+                    c->ring,   c->state, c->r,     c->sigma, c->e,       c->e_tmp,   c->sweeps,
+                    c->conv,   c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    c->flags};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int sslg_get_config(const sslg_ctx* c, sslg_config* cfg) {
+    if (!c || !cfg) return set_err(SSLG_VALIDATION, "null argument");
+    *cfg = c->cfg;
+    cfg->dirs = c->dirs;
+    return SSLG_OK;
+}
+
+int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* bad_bin) {
+    if (!c || !k) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t mm = (size_t)g.m * g.m;
+    const size_t n = g.bins * mm * 2;
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(k[i])) return set_err(SSLG_VALIDATION, "non-finite correlation entry");
+    CU(cudaMemcpyAsync(c->k, k, g.bins * mm * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    TRY(reset_flags(c));
+    unsigned int fl[5];
+    if (check_pd) {
+        launch_pd_check(c->k, (int)g.m, (int)g.bins, c->flags + 3, c->flags + 4, nullptr, c->stream);
+        TRY(check_last_launch("pd_check_kernel"));
+        TRY(sync_flags(c, fl, 5));
+        if (fl[3] != 0xffffffffu || fl[4] != 0xffffffffu) {
+            c->have_noise = false;
+            const bool herm_first = fl[3] <= fl[4];
+            const unsigned b = herm_first ? fl[3] : fl[4];
+            if (bad_bin) *bad_bin = b;
+            return set_err(SSLG_NUMERICAL, std::string(herm_first ? "noise model is not Hermitian at bin "
+                                                                  : "noise model is not positive definite at bin ") +
+                                               std::to_string(b));
+        }
+    }
+    if (!g.pivoting)
+        return set_err(SSLG_VALIDATION, "pivot-free inversion is not supported by the device engine");
+    launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, c->kinv, c->flags + 1, c->flags + 2, c->stream);
+    TRY(check_last_launch("gauss_jordan_kernel"));
+    TRY(sync_flags(c, fl, 3));
+    const unsigned bad = std::min(fl[1], fl[2]);
+    if (bad != 0xffffffffu) {
+        c->have_noise = false;
+        if (bad_bin) *bad_bin = bad;
+        return set_err(SSLG_NUMERICAL, "noise matrix is singular at bin " + std::to_string(bad));
+    }
+    c->have_noise = true;
+    return SSLG_OK;
+}
+
+int sslg_set_noise_identity(sslg_ctx* c) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    const size_t mm = (size_t)c->cfg.m * c->cfg.m;
+    std::vector<float> k(c->cfg.bins * mm * 2, 0.0f);
+    for (size_t b = 0; b < c->cfg.bins; ++b)
+        for (size_t i = 0; i < c->cfg.m; ++i) k[(b * mm + i * c->cfg.m + i) * 2] = 1.0f;
+    return sslg_set_noise_model(c, k.data(), 0, nullptr);
+}
+
+int sslg_build_topology(const double* dirs_deg, uint32_t n, double radius_deg, uint32_t* nbr_off, uint32_t* nbr,
+                        uint32_t cap, uint32_t* nnz) {
+    // DirectionTopology::build (music.cpp:176-195): unit vectors in FP64,
+    // neighbors where the dot product reaches cos(radius)
+    const double pi = 3.14159265358979323846;
+    std::vector<double> u(3 * (size_t)n);
+    for (uint32_t i = 0; i < n; ++i) {
+        const double az = dirs_deg[2 * i] * pi / 180.0;
+        const double el = dirs_deg[2 * i + 1] * pi / 180.0;
+        u[3 * i] = std::cos(el) * std::cos(az);
+        u[3 * i + 1] = std::cos(el) * std::sin(az);
+        u[3 * i + 2] = std::sin(el);
+    }
+    const double cr = std::cos(radius_deg * pi / 180.0);
+    std::vector<std::vector<uint32_t>> lists(n);
+    for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t j = i + 1; j < n; ++j) {
+            const double dot = u[3 * i] * u[3 * j] + u[3 * i + 1] * u[3 * j + 1] + u[3 * i + 2] * u[3 * j + 2];
+            if (dot >= cr) {
+                lists[i].push_back(j);
+                lists[j].push_back(i);
+            }
+        }
+    uint32_t total = 0;
+    for (uint32_t i = 0; i < n; ++i) total += (uint32_t)lists[i].size();
+    if (nnz) *nnz = total;
+    if (total > cap || !nbr_off || (!nbr && total))
+        return set_err(SSLG_VALIDATION, "topology capacity too small: need " + std::to_string(total));
+    uint32_t o = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        nbr_off[i] = o;
+        for (uint32_t j : lists[i]) nbr[o++] = j;
+    }
+    nbr_off[n] = o;
+    return SSLG_OK;
+}
+
+int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* dirs_deg, const uint32_t* nbr_off,
+                      const uint32_t* nbr) {
+    if (!c || !h) return set_err(SSLG_VALIDATION, "null argument");
+    if (dirs == 0) return set_err(SSLG_VALIDATION, "steering field has no directions");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    std::vector<uint32_t> off_own, nbr_own;
+    if (!nbr_off) {
+        if (!dirs_deg) return set_err(SSLG_VALIDATION, "directions are needed to build the topology");
+        uint32_t need = 0;
+        off_own.resize(dirs + 1);
+        sslg_build_topology(dirs_deg, dirs, 10.0, off_own.data(), nullptr, 0, &need);
+        nbr_own.resize(std::max<uint32_t>(need, 1));
+        TRY(sslg_build_topology(dirs_deg, dirs, 10.0, off_own.data(), nbr_own.data(), need, &need));
+        nbr_off = off_own.data();
+        nbr = nbr_own.data();
+    }
+    const uint32_t nnz = nbr_off[dirs];
+    for (uint32_t d = 0; d < dirs; ++d)
+        if (nbr_off[d] > nbr_off[d + 1]) return set_err(SSLG_VALIDATION, "neighbor offsets must be non-decreasing");
+    for (uint32_t k = 0; k < nnz; ++k)
+        if (nbr[k] >= dirs) return set_err(SSLG_VALIDATION, "neighbor index out of range");
+    const size_t hn = (size_t)dirs * g.bins * g.m;
+    for (size_t i = 0; i < 2 * hn; ++i)
+        if (!std::isfinite(h[i])) return set_err(SSLG_VALIDATION, "non-finite steering value");
+    if (dirs != c->dirs) {
+        for (void* p : {(void*)c->h_raw, (void*)c->h_t, (void*)c->num, (void*)c->p, (void*)c->power,
+                        (void*)c->est_idx, (void*)c->est_pw, (void*)c->est_low})
+            if (p) cudaFree(p);
+        c->h_raw = c->h_t = nullptr;
+        c->num = c->p = c->power = c->est_pw = nullptr;
+        c->est_idx = nullptr;
+        c->est_low = nullptr;
+        const size_t NB = g.max_batch;
+        TRY(dalloc(&c->h_raw, hn));
+        TRY(dalloc(&c->h_t, hn));
+        TRY(dalloc(&c->num, (size_t)g.bins * dirs));
+        TRY(dalloc(&c->p, NB * g.bins * dirs));
+        TRY(dalloc(&c->power, NB * dirs));
+        TRY(dalloc(&c->est_idx, NB * g.num_sources));
+        TRY(dalloc(&c->est_pw, NB * g.num_sources));
+        TRY(dalloc(&c->est_low, NB * g.num_sources));
+        c->dirs = dirs;
+    }
+    if (c->nbr_off) cudaFree(c->nbr_off);
+    if (c->nbr) cudaFree(c->nbr);
+    c->nbr_off = c->nbr = nullptr;
+    TRY(dalloc(&c->nbr_off, dirs + 1));
+    TRY(dalloc(&c->nbr, std::max<uint32_t>(nnz, 1)));
+    c->nnz = nnz;
+    CU(cudaMemcpyAsync(c->nbr_off, nbr_off, (dirs + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (nnz) CU(cudaMemcpyAsync(c->nbr, nbr, nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->h_raw, h, hn * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    launch_steering_prep(c->h_raw, c->h_t, c->num, (int)g.m, (int)g.bins, (int)dirs, c->stream);
+    TRY(check_last_launch("steering_prep_kernel"));
+    CU(cudaStreamSynchronize(c->stream));
+    c->have_steering = true;
+    return SSLG_OK;
+}
+
+int sslg_reset_window(sslg_ctx* c) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
+    CU(cudaMemsetAsync(c->state, 0, (size_t)c->cfg.bins * c->cfg.m * c->cfg.m * sizeof(double2), c->stream));
+    c->pushed = 0;
+    c->since = 0;
+    c->last_emitted = 0;
+    return SSLG_OK;
+}
+
+int sslg_synchronize(sslg_ctx* c) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaStreamSynchronize(c->stream));
+    return SSLG_OK;
+}
+
+int sslg_push_frames_device(sslg_ctx* c, const void* x_dev, uint32_t nframes, uint32_t* emitted) {
+    TRY(require_ready(c));
+    c->launches = 0;
+    uint32_t total = 0;
+    if (nframes > c->cfg.max_batch)
+        return set_err(SSLG_VALIDATION, "push larger than max_batch; split it or raise max_batch");
+    TRY(stage_frames(c, static_cast<const float*>(x_dev), nframes, cudaMemcpyDeviceToDevice));
+    TRY(process_chunk(c, nframes, &total));
+    if (emitted) *emitted = total;
+    return SSLG_OK;
+}
+
+int sslg_read_results(sslg_ctx* c, uint32_t n, sslg_block_out* blocks, uint32_t* est_idx, double* est_power,
+                      uint8_t* est_low, double* power, double* bin_power, double* sigma, uint32_t* sweeps,
+                      uint8_t* conv) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
+    if (n > c->last_emitted) return set_err(SSLG_VALIDATION, "fewer blocks available than requested");
+    const sslg_config& g = c->cfg;
+    const size_t ns = g.num_sources, D = c->dirs, B = g.bins;
+    std::vector<uint32_t> cnt(n);
+    if (n) CU(cudaMemcpyAsync(cnt.data(), c->est_count, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (est_idx && n) CU(cudaMemcpyAsync(est_idx, c->est_idx, n * ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (est_power && n) CU(cudaMemcpyAsync(est_power, c->est_pw, n * ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (est_low && n) CU(cudaMemcpyAsync(est_low, c->est_low, n * ns, cudaMemcpyDeviceToHost, c->stream));
+    if (power && n) CU(cudaMemcpyAsync(power, c->power, n * D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (bin_power && n) CU(cudaMemcpyAsync(bin_power, c->p, n * B * D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (sigma && n) CU(cudaMemcpyAsync(sigma, c->sigma, n * B * g.m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (sweeps && n) CU(cudaMemcpyAsync(sweeps, c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (conv && n) CU(cudaMemcpyAsync(conv, c->conv, n * B, cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (blocks)
+        for (uint32_t i = 0; i < n; ++i) {
+            blocks[i].frame_index = (uint32_t)(c->last_first_frame + i);
+            blocks[i].count = cnt[i];
+        }
+    return SSLG_OK;
+}
+
+int sslg_push_frames(sslg_ctx* c, const float* x, uint32_t nframes, sslg_block_out* blocks, uint32_t* est_idx,
+                     double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    TRY(require_ready(c));
+    const sslg_config& g = c->cfg;
+    const size_t fsz = (size_t)g.m * g.bins * 2;
+    const size_t ns = g.num_sources;
+    uint32_t out = 0, done = 0, launches = 0;
+    while (done < nframes) {
+        const uint32_t chunk = std::min<uint32_t>(nframes - done, g.max_batch);
+        c->launches = 0;
+        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice));
+        uint32_t e = 0;
+        TRY(process_chunk(c, chunk, &e));
+        launches += c->launches;
+        TRY(sslg_read_results(c, e, blocks ? blocks + out : nullptr, est_idx ? est_idx + out * ns : nullptr,
+                              est_power ? est_power + out * ns : nullptr, est_low ? est_low + out * ns : nullptr,
+                              power ? power + (size_t)out * c->dirs : nullptr, nullptr, nullptr, nullptr, nullptr));
+        out += e;
+        done += chunk;
+    }
+    c->launches = launches;
+    if (emitted) *emitted = out;
+    return SSLG_OK;
+}
+
+int sslg_correlation(sslg_ctx* c, const float* x, uint32_t nframes, float* r_out, uint32_t* emitted) {
+    if (!c || !x) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t fsz = (size_t)g.m * g.bins * 2;
+    const size_t rsz = (size_t)g.bins * g.m * g.m;
+    uint32_t out = 0, done = 0;
+    c->launches = 0;
+    while (done < nframes) {
+        const uint32_t chunk = std::min<uint32_t>(nframes - done, g.max_batch);
+        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice));
+        const long long first_emit = std::max<long long>(0, (long long)g.window_frames - 1 - c->pushed);
+        const int n = (int)std::max<long long>(0, (long long)chunk - first_emit);
+        CorrArgs ca{c->ring, c->state, c->r, (int)g.m, (int)g.bins, (int)g.window_frames, c->cap, (int)chunk,
+                    c->pushed, c->since, (int)g.rebuild_interval};
+        launch_correlation(ca, c->stream);
+        ++c->launches;
+        TRY(check_last_launch("correlation_kernel"));
+        for (uint32_t f = 0; f < chunk; ++f) {
+            ++c->pushed;
+            if (++c->since >= (long long)g.rebuild_interval) c->since = 0;
+        }
+        if (n > 0 && r_out)
+            CU(cudaMemcpyAsync(r_out + out * rsz * 2, c->r, n * rsz * sizeof(float2), cudaMemcpyDeviceToHost,
+                               c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        out += (uint32_t)n;
+        done += chunk;
+    }
+    if (emitted) *emitted = out;
+    return SSLG_OK;
+}
+
+int sslg_gsvd(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, double* e, uint32_t* sweeps,
+              uint8_t* conv) {
+    if (!c || !r) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model not set");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t mm = (size_t)g.m * g.m, B = g.bins;
+    for (size_t i = 0; i < (size_t)nsets * B * mm * 2; ++i)
+        if (!std::isfinite(r[i])) return set_err(SSLG_VALIDATION, "non-finite correlation entry");
+    c->launches = 0;
+    for (uint32_t done = 0; done < nsets;) {
+        const uint32_t n = std::min<uint32_t>(nsets - done, g.max_batch);
+        CU(cudaMemcpyAsync(c->r, r + (size_t)done * B * mm * 2, n * B * mm * sizeof(float2), cudaMemcpyHostToDevice,
+                           c->stream));
+        CU(cudaEventRecord(c->ev[1], c->stream));
+        TRY(run_gsvd(c, (int)n));
+        if (e) {
+            const size_t tot = n * B * mm;
+            transpose_sq_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(c->e, c->e_tmp, (int)g.m, n * B);
+            ++c->launches;
+            TRY(check_last_launch("transpose_sq_kernel"));
+            CU(cudaMemcpyAsync(e + (size_t)done * B * mm * 2, c->e_tmp, tot * sizeof(double2), cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
+        if (sigma)
+            CU(cudaMemcpyAsync(sigma + (size_t)done * B * g.m, c->sigma, n * B * g.m * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+        if (sweeps)
+            CU(cudaMemcpyAsync(sweeps + (size_t)done * B, c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+        if (conv) CU(cudaMemcpyAsync(conv + (size_t)done * B, c->conv, n * B, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        done += n;
+    }
+    return SSLG_OK;
+}
+
+int sslg_spectrum(sslg_ctx* c, const double* e, uint32_t nsets, double* power, double* bin_power) {
+    if (!c || !e) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
+    if (c->cfg.num_sources >= c->cfg.m)
+        return set_err(SSLG_VALIDATION, "num_sources must be smaller than the channel count");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t mm = (size_t)g.m * g.m, B = g.bins, D = c->dirs;
+    c->launches = 0;
+    for (uint32_t done = 0; done < nsets;) {
+        const uint32_t n = std::min<uint32_t>(nsets - done, g.max_batch);
+        const size_t tot = n * B * mm;
+        CU(cudaMemcpyAsync(c->e_tmp, e + (size_t)done * B * mm * 2, tot * sizeof(double2), cudaMemcpyHostToDevice,
+                           c->stream));
+        transpose_sq_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(c->e_tmp, c->e, (int)g.m, n * B);
+        ++c->launches;
+        TRY(check_last_launch("transpose_sq_kernel"));
+        TRY(run_music(c, (int)n));
+        if (power)
+            CU(cudaMemcpyAsync(power + (size_t)done * D, c->power, n * D * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+        if (bin_power)
+            CU(cudaMemcpyAsync(bin_power + (size_t)done * B * D, c->p, n * B * D * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        done += n;
+    }
+    return SSLG_OK;
+}
+
+int sslg_peaks(sslg_ctx* c, const double* power, uint32_t nsets, uint32_t* est_idx, double* est_power,
+               uint8_t* est_low, uint32_t* count) {
+    if (!c || !power) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t D = c->dirs, ns = g.num_sources;
+    c->launches = 0;
+    for (uint32_t done = 0; done < nsets;) {
+        const uint32_t n = std::min<uint32_t>(nsets - done, g.max_batch);
+        // integrate over a single "bin" holding the given broadband power
+        CU(cudaMemcpyAsync(c->p, power + (size_t)done * D, n * D * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        PeakArgs pa{c->p, c->power, c->nbr_off, c->nbr, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    1, (int)D, (int)ns, (double)g.low_power_ratio};
+        launch_peaks(pa, (int)n, c->stream);
+        ++c->launches;
+        TRY(check_last_launch("integrate_peaks_kernel"));
+        if (est_idx) CU(cudaMemcpyAsync(est_idx + done * ns, c->est_idx, n * ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        if (est_power) CU(cudaMemcpyAsync(est_power + done * ns, c->est_pw, n * ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (est_low) CU(cudaMemcpyAsync(est_low + done * ns, c->est_low, n * ns, cudaMemcpyDeviceToHost, c->stream));
+        if (count) CU(cudaMemcpyAsync(count + done, c->est_count, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        done += n;
+    }
+    return SSLG_OK;
+}
+
+int sslg_last_stage_ms(const sslg_ctx* c, float* ms5) {
+    if (!c || !ms5) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->timed) return set_err(SSLG_VALIDATION, "nothing timed yet");
+    for (int i = 0; i < 5; ++i) {
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, c->ev[i], c->ev[i + 1]));
+        ms5[i] = ms;
+    }
+    return SSLG_OK;
+}
+
+uint32_t sslg_last_launch_count(const sslg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Launch interfaces of the sm_100a kernels, shared by the kernel translation
+// units and the host engine (engine.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sslg {
+
+struct CorrArgs {
+    const float2* ring;  // [cap][m][bins] spectra, frame g at slot g % cap
+    double2* state;      // [bins][m][m] FP64 running sum
+    float2* r_out;       // [n_emit][bins][m][m]
+    int m, bins, t, cap;
+    int frames;          // frames ingested by this launch
+    long long pushed0;   // pushes before this launch (== global index of first frame)
+    long long since0;    // pushes since the last rebuild
+    int rebuild_interval;
+};
+void launch_correlation(const CorrArgs& a, cudaStream_t s);
+void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStream_t s);
+
+void launch_gauss_jordan(const float2* k, int m, int bins, double2* inv_out, unsigned int* bad_f,
+                         unsigned int* bad_d, cudaStream_t s);
+void launch_pd_check(const float2* k, int m, int bins, unsigned int* bad_herm, unsigned int* bad_pd,
+                     double* min_pivot, cudaStream_t s);
+
+struct GsvdArgs {
+    const float2* r;      // [nblk][bins][m][m] row-major R
+    const double2* kinv;  // [bins][m][m] row-major K^-1
+    double* sigma;        // [nblk][bins][m]
+    double2* e;           // [nblk][bins][m vec][m row]
+    uint32_t* sweeps;     // [nblk][bins]
+    uint8_t* conv;        // [nblk][bins]
+    int m, bins, max_sweeps;
+};
+void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
+
+struct CanonArgs {
+    const float2* r;      // [nblk][bins][m][m]
+    const double2* kinv;  // [bins][m][m]
+    const double* sigma;  // [nblk][bins][m]
+    double2* e;           // [nblk][bins][m vec][m row]  (in/out)
+    int m, bins, refine;
+};
+void launch_canonical(const CanonArgs& a, int nblk, cudaStream_t s);
+
+struct SpecArgs {
+    const double2* e;    // [nblk][bins][m vec][m mic]
+    const float2* h;     // [bins][dirs][m]
+    const double* num;   // [bins][dirs]  |h|^2
+    double* p;           // [nblk][bins][dirs]
+    int m, bins, dirs, ns, dchunk, nsplit;
+    double floor_;
+    int squared;
+};
+void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s);
+void launch_steering_prep(const float2* h_in, float2* h_t, double* num, int m, int bins, int dirs,
+                          cudaStream_t s);
+
+struct PeakArgs {
+    const double* p;          // [nblk][bins][dirs]
+    double* power;            // [nblk][dirs]
+    const uint32_t* nbr_off;  // [dirs + 1]
+    const uint32_t* nbr;      // [nnz]
+    uint32_t* est_idx;        // [nblk][ns]
+    double* est_pw;           // [nblk][ns]
+    uint8_t* est_low;         // [nblk][ns]
+    uint32_t* est_count;      // [nblk]
+    int bins, dirs, ns;
+    double low_ratio;         // double(float ratio)
+};
+void launch_peaks(const PeakArgs& a, int nblk, cudaStream_t s);
+
+}  // namespace sslg
