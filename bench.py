@@ -1,0 +1,442 @@
+#!/usr/bin/env python
+"""Throughput of the B200 GSVD-MUSIC hot path (BASELINE.json metric):
+60-ch GSVD-MUSIC SSL blocks/sec, GSVD latency per block (us), x real-time.
+
+Workload (BASELINE.json configs[2], "C3"): 60-ch circular array (r = 0.3 m),
+16 kHz, 512-pt FFT -> 257 bins, 72 azimuths, two targets under four rotor
+noise sources + diffuse floor, K captured from noise-only frames, T = 50,
+Ns = 2.  Synthetic STFT-domain frames (paper_2504_03373_b200/synth.py).
+
+One step = one pass of the hot path over one batch of `--batch` new STFT
+frames per GPU = `--batch` blocks (the window is kept full), each block being
+correlation update + GSVD over 257 bins + MUSIC over 72 x 257 + integration +
+peak search.  N > 1: one independent array (stream) per GPU, no data-path
+collective ("scaling": "weak"); time = max over ranks of the device time.
+
+Arms:
+  default            this engine (libsslgpu.so); prints one JSON line
+  --impl reference   the reference's own CPU implementation (oracle/_ref, the
+                     unmodified sslkit library) on the host cores, same
+                     workload / metric; rank 0 only
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "60-ch GSVD-MUSIC SSL blocks/sec; GSVD latency per block (us); x real-time"
+UNIT = "blocks/s"
+REALTIME_BLOCKS_PER_S = 100.0  # fs / shift = 16000 / 160 per array
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--batch", type=int, default=32, help="blocks (new frames) per step per GPU")
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-blocks", type=int, default=48)
+    p.add_argument("--no-flush", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            self._ok = False
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self._ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self._ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self._ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per block (SURVEY.md §8(d) convention)
+# ---------------------------------------------------------------------------
+
+
+def algorithmic(m, bins, dirs, ns, t=50):
+    s_nom = 10
+    f_whiten = 8.0 * bins * m ** 3
+    f_jacobi = bins * s_nom * m * (m - 1) / 2 * 36 * m
+    f_music = 8.0 * dirs * bins * (m - ns) * m
+    corr_bytes = 2 * bins * m * 8 + bins * m * m * 8
+    spec_bytes = bins * (m - ns) * m * 16 + bins * dirs * m * 8 + bins * dirs * 8
+    return dict(f_whiten=f_whiten, f_jacobi=f_jacobi, f_music=f_music, corr_bytes=corr_bytes, spec_bytes=spec_bytes)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(path):
+        try:
+            with open(path) as f:
+                return json.load(f)
+        except Exception:
+            return None
+    return None
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm / cpu_baseline leg (oracle/_ref = the unmodified reference)
+# ---------------------------------------------------------------------------
+
+
+def reference_time_blocks(w, nblocks, threads):
+    """Times the reference's run_locate per-frame loop (pipeline.cpp:227-245,
+    batched float path, `threads` workers) over `nblocks` emitted blocks of the
+    workload; returns (seconds per block, stage seconds)."""
+    import oracle
+
+    R = oracle.ref()
+    frames = w.t - 1 + nblocks
+    wl = oracle.Workload(w.x[:frames], w.k, w.h, w.dirs)
+    mc = oracle.MusicCfg.make(num_sources=w.ns)
+    out = R.locate_frames(wl, w.t, mc, path=0, threads=threads)
+    st = out["stage_s"]
+    # stage clocks of the emitting frames: push + normalize + gsvd + spectrum
+    # + peaks per block (the T-1 window-filling pushes are not charged)
+    return float(np.sum(st)) / nblocks, st
+
+
+def run_reference_arm(args, w, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    per_step = max(1, min(args.batch, 4))
+    for _ in range(max(0, args.warmup)):
+        reference_time_blocks(w, per_step, cores)
+    times = []
+    for _ in range(args.steps):
+        spb, _ = reference_time_blocks(w, per_step, cores)
+        times.append(spb * per_step)
+    total = sum(times)
+    value = args.steps * per_step / total
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{w.name}: {w.m}-ch, {w.bins} bins, {w.h.shape[0]} dirs, T={w.t}, Ns={w.ns}",
+                   "blocks_per_step": per_step, "path": "ssl::gsvd batched float + calc_average_power<float>"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{per_step} blocks per step of the same C3 stream through the reference "
+                                   f"run_locate loop (oracle/_ref, {cores} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "x_realtime": value / REALTIME_BLOCKS_PER_S,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2504_03373_b200 import synth
+
+    frames_needed = 50 + (args.warmup + args.steps + 1) * args.batch
+    w = synth.make(args.config, frames=max(frames_needed, 120), seed=11 + rank)
+
+    if args.impl == "reference":
+        try:
+            import oracle
+
+            if not oracle.ref_available():
+                raise FileNotFoundError("oracle/_ref/libsslref.so missing")
+        except Exception as e:  # the reference arm is unavailable
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": str(e).splitlines()[0]}), flush=True)
+            return
+        run_reference_arm(args, w, rank, world)
+        return
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    device = local
+
+    from paper_2504_03373_b200 import _capi, ssl
+
+    # a dedicated stream: the engine launches on it and the CUDA events below
+    # are recorded on it (torch's default stream is the legacy NULL stream)
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
+    eng = ssl.Engine(w.m, w.bins, window_frames=w.t, music=ssl.MusicConfig(num_sources=w.ns),
+                     max_batch=args.batch, device=device, stream=stream.cuda_stream)
+    eng.set_noise_model(w.k)
+    eng.set_steering(w.h, w.dirs)
+
+    # inputs resident in HBM before the timed region
+    x_all = torch.from_numpy(w.x.view(np.float32)).to(f"cuda:{device}")  # [F][m][bins*2]
+    fsz = w.m * w.bins
+    pos = 0
+
+    def next_frames(n):
+        nonlocal pos
+        if pos + n > x_all.shape[0]:
+            pos = w.t  # recycle the pool after the fill
+        v = x_all[pos:pos + n]
+        pos += n
+        return v
+
+    # fill the window (frames 0..T-2), then one emitting push
+    left = w.t - 1
+    while left > 0:
+        nf = min(left, args.batch)
+        fill = next_frames(nf)
+        eng.push_device(fill.data_ptr(), nf)
+        left -= nf
+    flush_buf = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    def sync_all():
+        torch.cuda.synchronize(device)
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        xb = next_frames(args.batch)
+        eng.push_device(xb.data_ptr(), args.batch)
+    sync_all()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stage = np.zeros(5)
+    launches = 0
+    emitted = 0
+    with ClockSampler(device) as clk:
+        for i in range(args.steps):
+            xb = next_frames(args.batch)
+            if flush_buf is not None:
+                flush_buf.zero_()  # L2 flush between timed steps (outside the events)
+            ev[i][0].record(stream)
+            n = eng.push_device(xb.data_ptr(), args.batch)
+            ev[i][1].record(stream)
+            stream.synchronize()
+            stage += eng.stage_ms()
+            launches += eng.launch_count()
+            emitted += n
+        sync_all()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        e = torch.tensor([emitted], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        emitted_all = int(e.item())
+    else:
+        emitted_all = emitted
+    value = emitted_all / (total_ms * 1e-3)
+    res = eng.read_results(args.batch, sigma=False)
+    hits = float(np.mean([set(r[: c].tolist()) == set(w.targets) for r, c in zip(res["idx"], res["count"])]))
+
+    # single-block GSVD latency (one array, one block per launch)
+    lat = []
+    for _ in range(5):
+        xb = next_frames(1)
+        eng.push_device(xb.data_ptr(), 1)
+        eng.synchronize()
+        s = eng.stage_ms()
+        lat.append(1e3 * float(s[1] + s[2]))
+    gsvd_latency_us = float(np.median(lat))
+
+    # e2e: the public C-ABI entry with host buffers (pinned), H2D + D2H inside
+    pinned = torch.from_numpy(w.x.view(np.float32)).pin_memory()
+    e2e_ms = []
+    ns = w.ns
+    hpos = w.t
+    for i in range(args.warmup + args.steps):
+        if hpos + args.batch > pinned.shape[0]:
+            hpos = w.t
+        xh = pinned[hpos:hpos + args.batch].numpy().view(np.complex64)
+        hpos += args.batch
+        sync_all()
+        t0 = time.perf_counter()
+        out = eng.push(xh)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_ms.append(dt * 1e3)
+    e2e_total = float(sum(e2e_ms))
+    if dist is not None:
+        t = torch.tensor([e2e_total], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * args.steps * args.batch / (e2e_total * 1e-3)
+    h2d = args.batch * fsz * 8
+    d2h = args.batch * (ns * (4 + 8 + 1) + 8)
+
+    if rank == 0:
+        alg = algorithmic(w.m, w.bins, w.h.shape[0], w.ns, w.t)
+        blocks_per_launch = args.batch
+        jac_ms = stage[1] / args.steps
+        can_ms = stage[2] / args.steps
+        spec_ms = stage[3] / args.steps
+        corr_ms = stage[0] / args.steps
+        fp64 = ctypes_probe(device)
+        peaks, peak_kind = load_peaks()
+        achieved_tf = (alg["f_whiten"] + alg["f_jacobi"]) * blocks_per_launch / (jac_ms * 1e-3) / 1e12
+        traffic = load_traffic()
+        jac_traffic = traffic.get("jacobi_kernel", {}).get("dram_bytes_per_launch") if traffic else None
+        roofline = {
+            "kernel": "jacobi_kernel (FP64 one-sided Jacobi, A = K^-1 R fused)",
+            "bound": "fp64", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s",
+            "frac": achieved_tf / fp64 if fp64 else None, "traffic": jac_traffic,
+            "peak_kind": "measured in-run (DFMA microbenchmark, sslg_probe_fp64_tflops); "
+                         "MEASURED_PEAKS.json has no FP64 entry",
+            "flops_per_block": alg["f_whiten"] + alg["f_jacobi"],
+            "flop_convention": "SURVEY.md §8(d): 8*B*M^3 + B*10*M(M-1)/2*36M",
+        }
+        kernels = {
+            "correlation": {"ms_per_launch": corr_ms,
+                            "achieved_gbs": alg["corr_bytes"] * blocks_per_launch / (corr_ms * 1e-3) / 1e9,
+                            "peak_gbs": peaks.get("hbm_gbs"), "peak_kind": peak_kind},
+            "jacobi": {"ms_per_launch": jac_ms, "us_per_block": 1e3 * jac_ms / blocks_per_launch},
+            "canonical": {"ms_per_launch": can_ms, "us_per_block": 1e3 * can_ms / blocks_per_launch},
+            "spectrum": {"ms_per_launch": spec_ms,
+                         "achieved_gbs": alg["spec_bytes"] * blocks_per_launch / (spec_ms * 1e-3) / 1e9,
+                         "achieved_tflops": alg["f_music"] * blocks_per_launch / (spec_ms * 1e-3) / 1e12,
+                         "peak_gbs": peaks.get("hbm_gbs")},
+            "peaks": {"ms_per_launch": stage[4] / args.steps},
+        }
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(w, args.cpu_sample_blocks)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C3 (BASELINE configs[2]): {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, "
+                                   f"{w.bins} bins, {w.h.shape[0]} azimuths, 2 targets + 4 rotor sources + diffuse, "
+                                   f"captured K, T={w.t}, Ns={w.ns}",
+                       "blocks_per_step_per_gpu": args.batch, "arrays": world,
+                       "l2": "flushed (256 MiB write) between timed steps" if not args.no_flush else "not flushed",
+                       "parallelism": f"array-sharded x{world} (no data-path collective)"},
+            "gsvd_us_per_block": 1e3 * (jac_ms + can_ms) / blocks_per_launch,
+            "gsvd_latency_us_single_block": gsvd_latency_us,
+            "x_realtime": value / REALTIME_BLOCKS_PER_S,
+            "target_hit_rate": hits,
+            "roofline": roofline,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "sslg_push_frames (host buffers)"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def ctypes_probe(device):
+    import ctypes as C
+
+    from paper_2504_03373_b200 import _capi
+
+    out = C.c_double()
+    rc = _capi.load().sslg_probe_fp64_tflops(device, C.byref(out))
+    return out.value if rc == 0 else None
+
+
+def cpu_baseline(w, nblocks):
+    try:
+        import oracle
+
+        if not oracle.ref_available():
+            return None
+    except Exception:
+        return None
+    cores = os.cpu_count() or 1
+    spb, st = reference_time_blocks(w, nblocks, cores)
+    return {"value": 1.0 / spb, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{nblocks} consecutive blocks of the same C3 stream through the reference run_locate loop "
+                      f"(oracle/_ref = unmodified sslkit, ssl::gsvd batched float path, {cores} threads)",
+            "stage_s": {"correlation": st[0], "factorization": st[1], "spectrum": st[2], "peaks": st[3]},
+            "gsvd_us_per_block": 1e6 * st[1] / nblocks}
+
+
+if __name__ == "__main__":
+    main()

@@ -61,7 +61,9 @@ typedef struct sslg_config {
     float low_power_ratio;       /* MusicConfig::low_power_ratio, default 1.25 */
     int pivoting;                /* SolverConfig::pivoting: 0 none, 1 partial */
     int canonical_subspaces;     /* SolverConfig::canonical_subspaces */
-    int refine_leading;          /* A A^H sharpening of the kept span (gsvd.cpp:440-466), default 1 */
+    int refine_leading;          /* A A^H sharpening of the kept span (gsvd.cpp:440-466); default 0 =
+                                    canonicalize in the span of the FP64 Jacobi basis (fused), 1 =
+                                    the reference's full-space procedure (canonical_kernel) */
     uint32_t max_sweeps;         /* Jacobi sweep cap, 0 = 60 (jacobi_svd, gsvd.cpp:631) */
     uint32_t max_batch;          /* blocks (frames) processed per launch; sizes device buffers */
     int device;                  /* CUDA device ordinal */
@@ -167,6 +169,9 @@ int sslg_peaks(sslg_ctx* ctx, const double* power, uint32_t nsets, uint32_t* est
 int sslg_last_stage_ms(const sslg_ctx* ctx, float* ms5);
 /* Number of kernel launches issued by the last push / stage call. */
 uint32_t sslg_last_launch_count(const sslg_ctx* ctx);
+/* Measured FP64 FMA throughput of `device` (TFLOP/s): the roofline
+ * denominator for the FP64 solver kernels. */
+int sslg_probe_fp64_tflops(int device, double* tflops);
 
 #ifdef __cplusplus
 }

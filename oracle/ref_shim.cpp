@@ -608,12 +608,11 @@ SHIM_API int sslref_locate_frames(const float* x, std::uint32_t frames, std::uin
         std::uint32_t e_out = 0;
         double st[4] = {0, 0, 0, 0};
         for (std::uint32_t f = 0; f < frames; ++f) {
+            // stage clocks cover emitting frames only (steady-state per-block
+            // cost; the T-1 window-filling pushes are excluded)
             auto mark = clk::now();
             win.push(frame_from(x + std::size_t(f) * m * bins * 2, m, bins, f));
-            if (!win.filled()) {
-                st[0] += std::chrono::duration<double>(clk::now() - mark).count();
-                continue;
-            }
+            if (!win.filled()) continue;
             const auto r = win.normalized();
             st[0] += std::chrono::duration<double>(clk::now() - mark).count();
             ssl::MusicSpectrum spec;

@@ -76,6 +76,7 @@ EXPORTS = {
     "sslg_peaks": (C.c_int, [C.c_void_p, _f64p, C.c_uint32, _u32p, _f64p, _u8p, _u32p]),
     "sslg_last_stage_ms": (C.c_int, [C.c_void_p, _f32p]),
     "sslg_last_launch_count": (C.c_uint32, [C.c_void_p]),
+    "sslg_probe_fp64_tflops": (C.c_int, [C.c_int, _f64p]),
 }
 
 _lib = None

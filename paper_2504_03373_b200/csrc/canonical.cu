@@ -181,7 +181,17 @@ __global__ void __launch_bounds__(kCanThreads, 1) canonical_kernel(CanonArgs a) 
     __shared__ double s_nrm;
     __shared__ PickScratch ps;
 
-    const int blk = blockIdx.x;
+    // persistent CTAs drain the worklist of bins the Jacobi epilogue could not
+    // canonicalize (work[0] = count, work[1] = cursor, work[2..] = indices)
+    __shared__ int s_blk;
+    for (;;) {
+    if (threadIdx.x == 0) {
+        const unsigned i = atomicAdd(a.work + 1, 1u);
+        s_blk = i < a.work[0] ? (int)a.work[2 + i] : -1;
+    }
+    __syncthreads();
+    const int blk = s_blk;
+    if (blk < 0) break;
     const int bin = blk % a.bins;
     const int t = threadIdx.x;
     const double* sg = a.sigma + (size_t)blk * m;
@@ -357,6 +367,8 @@ __global__ void __launch_bounds__(kCanThreads, 1) canonical_kernel(CanonArgs a) 
     }
     __syncthreads();
     for (int e = t; e < mm; e += blockDim.x) eg[e] = Es[e];
+    __syncthreads();
+    }
 }
 
 size_t canonical_smem_bytes(int m) { return 3 * (size_t)m * m * sizeof(double2); }
@@ -364,7 +376,9 @@ size_t canonical_smem_bytes(int m) { return 3 * (size_t)m * m * sizeof(double2);
 void launch_canonical(const CanonArgs& a, int nblk, cudaStream_t s) {
     const size_t smem = canonical_smem_bytes(a.m);
     cudaFuncSetAttribute(canonical_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    canonical_kernel<<<nblk * a.bins, kCanThreads, smem, s>>>(a);
+    int grid = nblk * a.bins;
+    if (grid > 148) grid = 148;  // persistent: one CTA per SM drains the worklist
+    canonical_kernel<<<grid, kCanThreads, smem, s>>>(a);
 }
 
 }  // namespace sslg

@@ -103,6 +103,7 @@ struct sslg_ctx {
     double2* e_tmp = nullptr;
     uint32_t* sweeps = nullptr;
     uint8_t* conv = nullptr;
+    uint32_t* work = nullptr;  // generic-canonicalization worklist
     double* p = nullptr;
     double* power = nullptr;
     uint32_t* est_idx = nullptr;
@@ -158,14 +159,15 @@ int check_last_launch(const char* what) {
 // Runs GSVD -> (canonical) on n correlation sets already in c->r.
 int run_gsvd(sslg_ctx* c, int n) {
     const sslg_config& g = c->cfg;
-    GsvdArgs ga{c->r, c->kinv, c->sigma, c->e, c->sweeps, c->conv, (int)g.m, (int)g.bins,
-                g.max_sweeps ? (int)g.max_sweeps : 60};
+    CU(cudaMemsetAsync(c->work, 0, 2 * sizeof(uint32_t), c->stream));
+    GsvdArgs ga{c->r,   c->kinv, c->sigma, c->e, c->sweeps, c->conv, c->work, (int)g.m, (int)g.bins,
+                g.max_sweeps ? (int)g.max_sweeps : 60, g.canonical_subspaces, g.refine_leading};
     launch_jacobi(ga, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
     if (g.canonical_subspaces) {
-        CanonArgs ca{c->r, c->kinv, c->sigma, c->e, (int)g.m, (int)g.bins, g.refine_leading};
+        CanonArgs ca{c->r, c->kinv, c->sigma, c->e, c->work, (int)g.m, (int)g.bins, g.refine_leading};
         launch_canonical(ca, n, c->stream);
         ++c->launches;
         TRY(check_last_launch("canonical_kernel"));
@@ -275,7 +277,7 @@ void sslg_config_default(sslg_config* cfg) {
     cfg->low_power_ratio = 1.25f;
     cfg->pivoting = 1;
     cfg->canonical_subspaces = 1;
-    cfg->refine_leading = 1;
+    cfg->refine_leading = 0;
     cfg->max_sweeps = 0;
     cfg->max_batch = 16;
     cfg->device = 0;
@@ -327,6 +329,7 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     rc |= dalloc(&c->e_tmp, NB * B * mm);
     rc |= dalloc(&c->sweeps, NB * B);
     rc |= dalloc(&c->conv, NB * B);
+    rc |= dalloc(&c->work, NB * B + 2);
     rc |= dalloc(&c->est_count, NB);
     rc |= dalloc(&c->flags, 8);
     for (int i = 0; i < 6 && !rc; ++i)
@@ -347,7 +350,7 @@ void sslg_destroy(sslg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->k,      c->kinv,  c->h_raw, c->h_t,   c->num,     c->nbr_off, c->nbr,
                     c->ring,   c->state, c->r,     c->sigma, c->e,       c->e_tmp,   c->sweeps,
-                    c->conv,   c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    c->conv,   c->work, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
                     c->flags};
     for (void* p : ptrs)
         if (p) cudaFree(p);

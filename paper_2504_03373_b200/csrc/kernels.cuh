@@ -31,15 +31,18 @@ struct GsvdArgs {
     double2* e;           // [nblk][bins][m vec][m row]
     uint32_t* sweeps;     // [nblk][bins]
     uint8_t* conv;        // [nblk][bins]
+    uint32_t* work;       // generic-canonicalization worklist: [0] count, [1] cursor, [2..] indices
     int m, bins, max_sweeps;
+    int canonical, refine;
 };
 void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 
 struct CanonArgs {
-    const float2* r;      // [nblk][bins][m][m]
-    const double2* kinv;  // [bins][m][m]
-    const double* sigma;  // [nblk][bins][m]
-    double2* e;           // [nblk][bins][m vec][m row]  (in/out)
+    const float2* r;         // [nblk][bins][m][m]
+    const double2* kinv;     // [bins][m][m]
+    const double* sigma;     // [nblk][bins][m]
+    double2* e;              // [nblk][bins][m vec][m row]  (in/out)
+    uint32_t* work;          // worklist filled by jacobi_kernel (see GsvdArgs)
     int m, bins, refine;
 };
 void launch_canonical(const CanonArgs& a, int nblk, cudaStream_t s);

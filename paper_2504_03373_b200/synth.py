@@ -1,0 +1,141 @@
+"""Synthetic STFT-domain workloads for the bench (BASELINE.json configs).
+
+Builds, directly in the frequency domain, the inputs the hot path consumes:
+spectrum frames X [F][m][bins] (SpectrumFrame layout), a noise correlation K
+captured from noise-only frames, and the far-field steering table H
+[dirs][bins][m].  The array geometries, direction grids and steering formula
+follow the reference generators (ArrayGeometry::circular / spherical,
+azimuth_grid, make_steering: proj/src/synth.cpp:59-149) — computed in FP64,
+stored FP32 — so the GSVD sees the same structure as the reference's scenes
+(rank <= T correlation windows, directional rotor noise, diffuse floor).
+This is input tooling for measurement, not part of the hot path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+SPEED_OF_SOUND = 343.0
+
+
+def circular(count: int, radius: float) -> np.ndarray:
+    ang = 2.0 * np.pi * np.arange(count) / count
+    return np.stack([radius * np.cos(ang), radius * np.sin(ang), np.zeros(count)], 1)
+
+
+def spherical(count: int, radius: float) -> np.ndarray:
+    ga = np.pi * (3.0 - np.sqrt(5.0))
+    i = np.arange(count, dtype=np.float64)
+    z = 1.0 - 2.0 * (i + 0.5) / count
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    az = i * ga
+    return np.stack([radius * r * np.cos(az), radius * r * np.sin(az), radius * z], 1)
+
+
+def azimuth_grid(step_deg: float = 5.0) -> np.ndarray:
+    n = int(np.floor(360.0 / step_deg + 1e-9))
+    return np.stack([np.arange(n) * step_deg, np.zeros(n)], 1)
+
+
+def azel_grid(step_deg: float = 5.0, el_min=-90.0, el_max=90.0, el_step=10.0) -> np.ndarray:
+    ring = azimuth_grid(step_deg)
+    els = np.arange(el_min, el_max + 1e-9, el_step)
+    return np.concatenate([np.stack([ring[:, 0], np.full(len(ring), e)], 1) for e in els], 0)
+
+
+def unit(dirs_deg: np.ndarray) -> np.ndarray:
+    az = np.deg2rad(dirs_deg[:, 0])
+    el = np.deg2rad(dirs_deg[:, 1])
+    return np.stack([np.cos(el) * np.cos(az), np.cos(el) * np.sin(az), np.sin(el)], 1)
+
+
+def steering(mics: np.ndarray, dirs_deg: np.ndarray, bin_min: int, bin_max: int, frame_length: int = 512,
+             sample_rate: int = 16000) -> np.ndarray:
+    """[dirs][bins][m] complex64: exp(-j 2 pi f tau), tau = -(u.p)/c (synth.cpp:17-22)."""
+    u = unit(dirs_deg)
+    tau = -(u @ mics.T) / SPEED_OF_SOUND  # [dirs][m]
+    f = np.arange(bin_min, bin_max + 1, dtype=np.float64) * sample_rate / frame_length
+    ang = -2.0 * np.pi * f[None, :, None] * tau[:, None, :]
+    return (np.cos(ang) + 1j * np.sin(ang)).astype(np.complex64)
+
+
+@dataclass
+class Workload:
+    name: str
+    x: np.ndarray  # [F][m][bins] complex64
+    k: np.ndarray  # [bins][m][m] complex64
+    h: np.ndarray  # [dirs][bins][m] complex64
+    dirs: np.ndarray  # [dirs][2]
+    t: int
+    ns: int
+    targets: List[int] = field(default_factory=list)
+
+    @property
+    def m(self):
+        return self.x.shape[1]
+
+    @property
+    def bins(self):
+        return self.x.shape[2]
+
+
+def _field(rng, mics, src_dirs, levels_db, bins_idx, frames, frame_length, sample_rate, diffuse_db):
+    m = mics.shape[0]
+    nb = len(bins_idx)
+    x = np.zeros((frames, nb, m), np.complex128)
+    if len(src_dirs):
+        hs = steering(mics, np.asarray(src_dirs, np.float64), bins_idx[0], bins_idx[-1], frame_length,
+                      sample_rate).astype(np.complex128)  # [S][bins][m]
+        for s, lvl in enumerate(levels_db):
+            amp = 10 ** (lvl / 20.0) * np.sqrt(frame_length / 2.0)
+            g = (rng.standard_normal((frames, nb)) + 1j * rng.standard_normal((frames, nb))) * (amp / np.sqrt(2))
+            x += g[:, :, None] * hs[s][None]
+    if diffuse_db is not None:
+        amp = 10 ** (diffuse_db / 20.0) * np.sqrt(frame_length / 2.0)
+        x += (rng.standard_normal((frames, nb, m)) + 1j * rng.standard_normal((frames, nb, m))) * (amp / np.sqrt(2))
+    return x
+
+
+def drone_scene(name: str = "c3", m: int = 60, geometry: str = "circular", radius: float = 0.3,
+                bin_min: int = 0, bin_max: int = 256, dirs: np.ndarray = None, frames: int = 400, t: int = 50,
+                ns: int = 2, targets_deg: Sequence[float] = (40.0, 150.0), target_db: float = -3.0,
+                rotors_deg: Sequence[float] = (45.0, 135.0, 225.0, 315.0), rotor_db: float = 0.0,
+                diffuse_db: float = -20.0, noise_frames: int = 240, seed: int = 11, frame_length: int = 512,
+                sample_rate: int = 16000) -> Workload:
+    """Low-SNR drone-like scene (BASELINE configs 3-5): targets below four
+    rotor noise sources plus a diffuse floor; K is captured from noise-only
+    frames (the capture_noise_model procedure, synth.cpp:329-373)."""
+    rng = np.random.default_rng(seed)
+    mics = circular(m, radius) if geometry == "circular" else spherical(m, radius)
+    dirs = azimuth_grid(5.0) if dirs is None else dirs
+    bins_idx = np.arange(bin_min, bin_max + 1)
+    src = [(a, 0.0) for a in targets_deg] + [(a, 0.0) for a in rotors_deg]
+    lv = [target_db] * len(targets_deg) + [rotor_db] * len(rotors_deg)
+    x = _field(rng, mics, src, lv, bins_idx, frames, frame_length, sample_rate, diffuse_db)
+    noise = _field(rng, mics, [(a, 0.0) for a in rotors_deg], [rotor_db] * len(rotors_deg), bins_idx,
+                   noise_frames, frame_length, sample_rate, diffuse_db)
+    # K = mean x x^H over the noise-only frames, FP64 then narrowed
+    k = np.einsum("fbi,fbj->bij", noise, noise.conj()) / noise_frames
+    k = k.astype(np.complex64)
+    h = steering(mics, dirs, bin_min, bin_max, frame_length, sample_rate)
+    xs = np.ascontiguousarray(x.transpose(0, 2, 1)).astype(np.complex64)  # [F][m][bins]
+    tgt = [int(np.argmin(np.abs(dirs[:, 0] - a) + np.abs(dirs[:, 1]))) for a in targets_deg]
+    return Workload(name, xs, k, h, np.ascontiguousarray(dirs, np.float64), t, ns, tgt)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "c1": dict(m=8, radius=0.05, targets_deg=(40.0, 150.0), target_db=0.0, rotors_deg=(), diffuse_db=-20.0, ns=2),
+    "c2": dict(m=16, radius=0.05, targets_deg=(75.0, 200.0), target_db=0.0, rotors_deg=(300.0,), ns=2),
+    "c3": dict(m=60, radius=0.3, ns=2),
+    "c4": dict(m=60, radius=0.3, ns=3, targets_deg=(40.0, 150.0, 260.0)),
+}
+
+
+def make(config: str, frames: int = 400, seed: int = 11) -> Workload:
+    kw = dict(CONFIGS[config])
+    if config == "c4":
+        kw["dirs"] = azel_grid(5.0)
+    return drone_scene(name=config, frames=frames, seed=seed, **kw)
