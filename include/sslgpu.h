@@ -64,6 +64,9 @@ typedef struct sslg_config {
     int refine_leading;          /* A A^H sharpening of the kept span (gsvd.cpp:440-466); default 0 =
                                     canonicalize in the span of the FP64 Jacobi basis (fused), 1 =
                                     the reference's full-space procedure (canonical_kernel) */
+    int precondition;            /* 1 (default): Householder QR with column pivoting, Jacobi on R^H
+                                    (converges in ~8 instead of ~18 sweeps); 0: Jacobi on A as
+                                    jacobi_svd (gsvd.cpp:622-695) */
     uint32_t max_sweeps;         /* Jacobi sweep cap, 0 = 60 (jacobi_svd, gsvd.cpp:631) */
     uint32_t max_batch;          /* blocks (frames) processed per launch; sizes device buffers */
     int device;                  /* CUDA device ordinal */
@@ -172,6 +175,11 @@ uint32_t sslg_last_launch_count(const sslg_ctx* ctx);
 /* Measured FP64 FMA throughput of `device` (TFLOP/s): the roofline
  * denominator for the FP64 solver kernels. */
 int sslg_probe_fp64_tflops(int device, double* tflops);
+/* Diagnostics: SM clocks summed over all GSVD CTAs per solver phase
+ * (whiten, QR, sweeps, sigma/back-multiply, basis completion, canonical
+ * picker + phase, store) since the last reset; needs SSLG_PHASE_CLOCKS=1 in
+ * the environment when the context is created. */
+int sslg_debug_phase_clocks(sslg_ctx* ctx, double* out8, int reset);
 
 #ifdef __cplusplus
 }

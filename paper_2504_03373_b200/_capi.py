@@ -42,6 +42,7 @@ class Config(C.Structure):
         ("pivoting", C.c_int),
         ("canonical_subspaces", C.c_int),
         ("refine_leading", C.c_int),
+        ("precondition", C.c_int),
         ("max_sweeps", C.c_uint32),
         ("max_batch", C.c_uint32),
         ("device", C.c_int),
@@ -77,6 +78,7 @@ EXPORTS = {
     "sslg_last_stage_ms": (C.c_int, [C.c_void_p, _f32p]),
     "sslg_last_launch_count": (C.c_uint32, [C.c_void_p]),
     "sslg_probe_fp64_tflops": (C.c_int, [C.c_int, _f64p]),
+    "sslg_debug_phase_clocks": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
 }
 
 _lib = None

@@ -33,12 +33,37 @@ __device__ __forceinline__ double shfl_xor_d(double v, int m, unsigned mask = 0x
     return __shfl_xor_sync(mask, v, m);
 }
 
+// 1/sqrt(x) and 1/x for positive normal FP64 arguments: the MUFU seed
+// (rsqrt/rcp.approx.ftz.f64, ~2^-22 relative) refined by two Newton steps to
+// full precision, without the special-case paths of the library versions.
+// Used on the Jacobi rotation-parameter chain, which is latency-bound.
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double hx = 0.5 * x;
+    y = y * fma(-hx * y, y, 1.5);
+    y = y * fma(-hx * y, y, 1.5);
+    return y;
+}
+__device__ __forceinline__ double fast_rcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    return y;
+}
+
 // Lanes of the aligned W-lane group that contains this thread.  Reductions
 // over a group name only that group, so groups may diverge independently.
 template <int W>
 __device__ __forceinline__ unsigned group_mask() {
-    if (W >= 32) return 0xffffffffu;
-    return ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
+    if constexpr (W >= 32) {
+        return 0xffffffffu;
+    } else {
+        return ((1u << W) - 1u) << ((threadIdx.x & 31) & ~(W - 1));
+    }
 }
 
 template <int W>

@@ -104,6 +104,8 @@ struct sslg_ctx {
     uint32_t* sweeps = nullptr;
     uint8_t* conv = nullptr;
     uint32_t* work = nullptr;  // generic-canonicalization worklist
+    double2* ascratch = nullptr;  // A copies for the preconditioned back-multiply
+    long long* phase_clk = nullptr;  // solver phase clocks (SSLG_PHASE_CLOCKS=1)
     double* p = nullptr;
     double* power = nullptr;
     uint32_t* est_idx = nullptr;
@@ -161,7 +163,8 @@ int run_gsvd(sslg_ctx* c, int n) {
     const sslg_config& g = c->cfg;
     CU(cudaMemsetAsync(c->work, 0, 2 * sizeof(uint32_t), c->stream));
     GsvdArgs ga{c->r,   c->kinv, c->sigma, c->e, c->sweeps, c->conv, c->work, (int)g.m, (int)g.bins,
-                g.max_sweeps ? (int)g.max_sweeps : 60, g.canonical_subspaces, g.refine_leading};
+                g.max_sweeps ? (int)g.max_sweeps : 60, g.canonical_subspaces, g.refine_leading,
+                g.precondition, c->ascratch, c->phase_clk};
     launch_jacobi(ga, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("jacobi_kernel"));
@@ -278,6 +281,7 @@ void sslg_config_default(sslg_config* cfg) {
     cfg->pivoting = 1;
     cfg->canonical_subspaces = 1;
     cfg->refine_leading = 0;
+    cfg->precondition = 1;
     cfg->max_sweeps = 0;
     cfg->max_batch = 16;
     cfg->device = 0;
@@ -330,6 +334,11 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     rc |= dalloc(&c->sweeps, NB * B);
     rc |= dalloc(&c->conv, NB * B);
     rc |= dalloc(&c->work, NB * B + 2);
+    if (g.precondition) rc |= dalloc(&c->ascratch, NB * B * mm);
+    if (const char* pc = std::getenv("SSLG_PHASE_CLOCKS"); pc && pc[0] == '1') {
+        rc |= dalloc(&c->phase_clk, 8);
+        if (!rc) cudaMemset(c->phase_clk, 0, 8 * sizeof(long long));
+    }
     rc |= dalloc(&c->est_count, NB);
     rc |= dalloc(&c->flags, 8);
     for (int i = 0; i < 6 && !rc; ++i)
@@ -350,7 +359,7 @@ void sslg_destroy(sslg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->k,      c->kinv,  c->h_raw, c->h_t,   c->num,     c->nbr_off, c->nbr,
                     c->ring,   c->state, c->r,     c->sigma, c->e,       c->e_tmp,   c->sweeps,
-                    c->conv,   c->work, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    c->conv,   c->work, c->ascratch, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
                     c->flags};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -732,5 +741,16 @@ int sslg_last_stage_ms(const sslg_ctx* c, float* ms5) {
 }
 
 uint32_t sslg_last_launch_count(const sslg_ctx* c) { return c ? c->launches : 0; }
+
+int sslg_debug_phase_clocks(sslg_ctx* c, double* out8, int reset) {
+    if (!c || !out8) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->phase_clk) return set_err(SSLG_VALIDATION, "phase clocks disabled (set SSLG_PHASE_CLOCKS=1)");
+    long long h[8];
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaMemcpy(h, c->phase_clk, sizeof h, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
+    if (reset) CU(cudaMemset(c->phase_clk, 0, sizeof h));
+    return SSLG_OK;
+}
 
 }  // extern "C"

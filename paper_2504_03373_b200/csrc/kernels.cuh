@@ -34,6 +34,9 @@ struct GsvdArgs {
     uint32_t* work;       // generic-canonicalization worklist: [0] count, [1] cursor, [2..] indices
     int m, bins, max_sweeps;
     int canonical, refine;
+    int precondition;     // QR-preconditioned Jacobi (needs ascratch)
+    double2* ascratch;    // [nblk][bins][m][m] column-major copy of A (precondition)
+    long long* phase_clk; // optional [8] summed SM clocks per solver phase (diagnostics)
 };
 void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 

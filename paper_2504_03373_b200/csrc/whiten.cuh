@@ -7,6 +7,36 @@
 
 namespace sslg {
 
+constexpr int kWhitenBatch = 8;  // K^-1 loads in flight per thread
+
+// acc[u] += sum_k K^-1[i][k] R[k][j_u], K^-1 row i streamed from global in
+// batches of kWhitenBatch independent loads (the row is L2-resident; a
+// dependent load per k would serialize ~m L2 round trips per thread).
+template <typename ColFn>
+__device__ __forceinline__ void whiten_rows(const double2* __restrict__ krow, const float2* rs, int m, double2* acc,
+                                            ColFn col) {
+    for (int k0 = 0; k0 < m; k0 += kWhitenBatch) {
+        double2 kv[kWhitenBatch];
+#pragma unroll
+        for (int b = 0; b < kWhitenBatch; ++b) kv[b] = (k0 + b < m) ? __ldg(&krow[k0 + b]) : make_double2(0, 0);
+#pragma unroll
+        for (int b = 0; b < kWhitenBatch; ++b) {
+            const int k = k0 + b;
+            if (k < m) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = col(u);
+                    if (j >= 0) {
+                        const double2 r = f2d(rs[k * m + j]);
+                        acc[u].x = fma(kv[b].x, r.x, fma(-kv[b].y, r.y, acc[u].x));
+                        acc[u].y = fma(kv[b].x, r.y, fma(kv[b].y, r.x, acc[u].y));
+                    }
+                }
+            }
+        }
+    }
+}
+
 // A = K^-1 R into W (column-major), staging R as float2 in the upper half of
 // the W buffer (bytes [8 m^2, 16 m^2)).  Columns j < m/2 live entirely in the
 // lower half and are written as soon as they are formed; the remaining
@@ -24,20 +54,17 @@ __device__ __forceinline__ void form_whitened(const float2* __restrict__ rb, con
     const bool active = tid < m * parts;
     const int i = active ? tid / parts : 0;
     const int part = active ? tid % parts : 0;
+    const double2* krow = kb + (size_t)i * m;
     // pass 1: columns 0..jl-1, written directly
     if (active) {
         for (int j0 = part; j0 < jl; j0 += 8 * parts) {
             double2 acc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[u] = make_double2(0, 0);
-            for (int k = 0; k < m; ++k) {
-                const double2 kv = __ldg(&kb[i * m + k]);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j = j0 + u * parts;
-                    if (j < jl) acc[u] = cadd(acc[u], cmul(kv, f2d(rs[k * m + j])));
-                }
-            }
+            whiten_rows(krow, rs, m, acc, [&](int u) {
+                const int j = j0 + u * parts;
+                return j < jl ? j : -1;
+            });
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int j = j0 + u * parts;
@@ -49,16 +76,11 @@ __device__ __forceinline__ void form_whitened(const float2* __restrict__ rb, con
     double2 hold[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) hold[u] = make_double2(0, 0);
-    if (active) {
-        for (int k = 0; k < m; ++k) {
-            const double2 kv = __ldg(&kb[i * m + k]);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int j = jl + part + u * parts;
-                if (j < m) hold[u] = cadd(hold[u], cmul(kv, f2d(rs[k * m + j])));
-            }
-        }
-    }
+    if (active)
+        whiten_rows(krow, rs, m, hold, [&](int u) {
+            const int j = jl + part + u * parts;
+            return j < m ? j : -1;
+        });
     __syncthreads();
     if (active) {
 #pragma unroll
