@@ -358,7 +358,10 @@ def main():
         peaks, peak_kind = load_peaks()
         achieved_tf = (alg["f_whiten"] + alg["f_jacobi"]) * blocks_per_launch / (jac_ms * 1e-3) / 1e12
         traffic = load_traffic()
-        jac_traffic = traffic.get("jacobi_kernel", {}).get("dram_bytes_per_launch") if traffic else None
+        jac_traffic = None
+        if traffic and "jacobi_kernel" in traffic:  # ncu capture (--batch 8) scaled to this launch
+            t = traffic["jacobi_kernel"]
+            jac_traffic = t["dram_bytes_per_launch"] / t.get("blocks_per_launch", 8) * blocks_per_launch
         roofline = {
             "kernel": "jacobi_kernel (FP64 one-sided Jacobi, A = K^-1 R fused)",
             "bound": "fp64", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s",

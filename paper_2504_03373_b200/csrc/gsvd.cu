@@ -246,7 +246,9 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
     if (t < m) qs.piv[t] = t;
     __syncthreads();
     for (int k = 0; k < m; ++k) {
-        if (warp == 0) {  // pivot: first column of largest remaining norm
+        // warp 0 alone: pivot (first column of largest remaining norm), column
+        // swap, and the reflector H = I - tau u u^H with H x = beta e_k
+        if (warp == 0) {
             double best = -1;
             int bi = k;
             for (int j = k + lane; j < m; j += kWarp)
@@ -263,38 +265,42 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
                     bi = oi;
                 }
             }
-            if (lane == 0) qs.p = bi;
-        }
-        __syncthreads();
-        const int p = qs.p;
-        if (p != k) {
-            if (t < m) {
-                const double2 x = W[k * m + t];
-                W[k * m + t] = W[p * m + t];
-                W[p * m + t] = x;
-            }
-            if (t == 0) {
-                const double x = qs.nrm2[k];
-                qs.nrm2[k] = qs.nrm2[p];
-                qs.nrm2[p] = x;
-                const int i = qs.piv[k];
-                qs.piv[k] = qs.piv[p];
-                qs.piv[p] = i;
-            }
-            __syncthreads();
-        }
-        if (warp == 0) {  // reflector H = I - tau u u^H with H x = beta e_k
+            const int p = bi;
             double a2 = 0;
-            for (int i = k + lane; i < m; i += kWarp) a2 += cnorm(W[k * m + i]);
+            for (int i = lane; i < m; i += kWarp) {
+                double2 xk = W[k * m + i];
+                if (p != k) {
+                    const double2 xp = W[p * m + i];
+                    W[p * m + i] = xk;
+                    W[k * m + i] = xp;
+                    xk = xp;
+                }
+                if (i >= k) a2 = fma(xk.x, xk.x, fma(xk.y, xk.y, a2));
+            }
             a2 = group_sum<kWarp>(a2);
+            __syncwarp();
             if (lane == 0) {
+                if (p != k) {
+                    const double x = qs.nrm2[k];
+                    qs.nrm2[k] = qs.nrm2[p];
+                    qs.nrm2[p] = x;
+                    const int i = qs.piv[k];
+                    qs.piv[k] = qs.piv[p];
+                    qs.piv[p] = i;
+                }
                 const double2 x0 = W[k * m + k];
                 const double alpha = sqrt(a2);
-                const double ax0 = hypot(x0.x, x0.y);
-                const double2 ph = ax0 > 0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+                const double ax2 = fma(x0.x, x0.x, x0.y * x0.y);
+                double2 ph = make_double2(1.0, 0.0);
+                double ax0 = 0.0;
+                if (ax2 > 0) {
+                    const double ri = fast_rsqrt(ax2);
+                    ax0 = ax2 * ri;
+                    ph = make_double2(x0.x * ri, x0.y * ri);
+                }
                 qs.beta = make_double2(-ph.x * alpha, -ph.y * alpha);
                 qs.u0 = make_double2(x0.x + ph.x * alpha, x0.y + ph.y * alpha);
-                qs.tau = alpha > 0 ? 1.0 / (alpha * (alpha + ax0)) : 0.0;
+                qs.tau = alpha > 0 ? fast_rcp(alpha * (alpha + ax0)) : 0.0;
             }
         }
         __syncthreads();
@@ -727,7 +733,9 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         cs.eligible = a.canonical && !a.refine && clean && dmax <= kZMax && m <= 64;
     }
     __syncthreads();
-    if (cs.eligible && cs.ndropped > 0) complete_basis(W, m, cs);
+    // the preconditioned vectors are re-orthonormalized whichever kernel
+    // canonicalizes them (the generic one reads the lead vectors too)
+    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis(W, m, cs);
     mark(4);
     const bool fused = cs.eligible;
     if (a.canonical && fused) {
