@@ -136,6 +136,14 @@ int sslg_push_frames_device(sslg_ctx* ctx, const void* x_dev, uint32_t nframes, 
 int sslg_read_results(sslg_ctx* ctx, uint32_t n, sslg_block_out* blocks, uint32_t* est_idx, double* est_power,
                       uint8_t* est_low, double* power, double* bin_power, double* sigma, uint32_t* sweeps,
                       uint8_t* conv);
+/* Bin sharding across GPUs (one array's bins split over ranks): copies the
+ * per-bin powers P [n][bins][dirs] f64 of the last push's first n blocks to
+ * the device buffer `dst` (stream-ordered on the context stream). */
+int sslg_copy_bin_power_device(sslg_ctx* ctx, void* dst, uint32_t n);
+/* Integration + peak search (music.cpp:143-160, 197-236) of externally
+ * assembled per-bin powers p_dev [n][bins_total][dirs] f64 (device), summed
+ * in ascending bin order; results are read with sslg_read_results. */
+int sslg_integrate_peaks_device(sslg_ctx* ctx, const void* p_dev, uint32_t n, uint32_t bins_total);
 /* Clears the correlation window (a fresh CorrelationWindow). */
 int sslg_reset_window(sslg_ctx* ctx);
 /* Blocks until the context stream is idle. */

@@ -69,6 +69,8 @@ EXPORTS = {
     "sslg_push_frames_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, _u32p]),
     "sslg_read_results": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(BlockOut), _u32p, _f64p, _u8p, _f64p, _f64p,
                                     _f64p, _u32p, _u8p]),
+    "sslg_copy_bin_power_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
+    "sslg_integrate_peaks_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32]),
     "sslg_reset_window": (C.c_int, [C.c_void_p]),
     "sslg_synchronize": (C.c_int, [C.c_void_p]),
     "sslg_correlation": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f32p, _u32p]),

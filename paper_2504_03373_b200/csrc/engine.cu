@@ -742,6 +742,33 @@ int sslg_last_stage_ms(const sslg_ctx* c, float* ms5) {
 
 uint32_t sslg_last_launch_count(const sslg_ctx* c) { return c ? c->launches : 0; }
 
+int sslg_copy_bin_power_device(sslg_ctx* c, void* dst, uint32_t n) {
+    if (!c || !dst) return set_err(SSLG_VALIDATION, "null argument");
+    if (n > c->last_emitted) return set_err(SSLG_VALIDATION, "fewer blocks available than requested");
+    CU(cudaSetDevice(c->cfg.device));
+    const size_t bytes = (size_t)n * c->cfg.bins * c->dirs * sizeof(double);
+    if (bytes) CU(cudaMemcpyAsync(dst, c->p, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    return SSLG_OK;
+}
+
+int sslg_integrate_peaks_device(sslg_ctx* c, const void* p_dev, uint32_t n, uint32_t bins_total) {
+    if (!c || !p_dev) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
+    if (n > c->cfg.max_batch) return set_err(SSLG_VALIDATION, "more blocks than max_batch");
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    c->launches = 0;
+    CU(cudaEventRecord(c->ev[4], c->stream));
+    PeakArgs pa{static_cast<const double*>(p_dev), c->power, c->nbr_off, c->nbr, c->est_idx, c->est_pw, c->est_low,
+                c->est_count, (int)bins_total, (int)c->dirs, (int)g.num_sources, (double)g.low_power_ratio};
+    launch_peaks(pa, (int)n, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("integrate_peaks_kernel"));
+    CU(cudaEventRecord(c->ev[5], c->stream));
+    c->last_emitted = n;
+    return SSLG_OK;
+}
+
 int sslg_debug_phase_clocks(sslg_ctx* c, double* out8, int reset) {
     if (!c || !out8) return set_err(SSLG_VALIDATION, "null argument");
     if (!c->phase_clk) return set_err(SSLG_VALIDATION, "phase clocks disabled (set SSLG_PHASE_CLOCKS=1)");

@@ -314,6 +314,14 @@ class Engine:
                     count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx, power_est=pw,
                     low=low.astype(bool), power=P, bin_power=BP, sigma=S, sweeps=sw, conv=cv.astype(bool))
 
+    def copy_bin_power_device(self, dst_ptr: int, n: int) -> None:
+        """Per-bin powers [n][bins][dirs] f64 of the last push -> device buffer."""
+        _capi.check(self.L.sslg_copy_bin_power_device(self.h, C.c_void_p(dst_ptr), n))
+
+    def integrate_peaks_device(self, p_ptr: int, n: int, bins_total: int) -> None:
+        """Ordered integration + peaks of assembled powers [n][bins_total][dirs] (device)."""
+        _capi.check(self.L.sslg_integrate_peaks_device(self.h, C.c_void_p(p_ptr), n, bins_total))
+
     def reset_window(self):
         _capi.check(self.L.sslg_reset_window(self.h))
 
