@@ -39,8 +39,11 @@ namespace sslg {
 constexpr int kLPP = SSLG_JAC_LPP;   // lanes per column pair
 constexpr int kJacThreads = 32 * kLPP;  // 32 column-pair groups
 constexpr int kRows = kMaxM / kLPP;  // rows per lane (8)
+constexpr double kReorth = 1e-5;  // re-orthonormalization line (relative to sigma_max)
 constexpr int kZMax = 24;            // largest group handled by the fused picker
 constexpr int kYld = kZMax + 1;      // padded row stride of the coordinate buffer
+// scratch after W: picker coordinates, C^H D products and the packed D^H D
+constexpr int kScratch = kMaxM * (kMaxM + 1) / 2 > kMaxM * kYld ? kMaxM * (kMaxM + 1) / 2 : kMaxM * kYld;
 
 struct CanonScratch {
     double nrm[kMaxM];
@@ -51,66 +54,143 @@ struct CanonScratch {
     int groups[kMaxM][2];     // rank ranges of tied groups
     double2 up[kMaxM];        // phase factor per rank
     unsigned ball[2];
-    int cert[kMaxM];          // column certified orthonormal to the others
     int dropped[kMaxM];       // columns below the final sweep's drop line
-    double2 dots[kMaxM];
-    double nrm1;
-    int ngroups, nvanish, eligible, ndropped;
+    int certcols[kMaxM];      // certified columns
+    double invd[kMaxM];       // 1 / L_jj of the CholeskyQR
+    int ngroups, nvanish, eligible, ndropped, ncert, collapsed;
 };
 
-// Completes the basis: every column below the drop line is orthonormalized
-// (two classical Gram-Schmidt passes) against all certified columns, then
-// certified itself.  Clears cs.eligible if a column collapses.
-__device__ void complete_basis(double2* W, int m, CanonScratch& cs) {
-    const int t = threadIdx.x;
-    const int k = t >> 2, part = t & 3;  // 4 lanes per column / row
-    for (int qd = 0; qd < cs.ndropped; ++qd) {
-        const int jd = cs.dropped[qd];
-        for (int pass = 0; pass < 2; ++pass) {
+// Completes the basis: the columns below the drop line (list D, rank order)
+// are orthonormalized against the certified columns C and then among
+// themselves.  Block form: two passes of D -= C (C^H D) (Gram product in the
+// scratch G, |C||D| <= m^2/4 entries), then one warp runs two classical
+// Gram-Schmidt passes per column of D against the earlier ones (8 dots per
+// butterfly) and normalizes it.  Clears cs.eligible if a column collapses.
+__device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) {
+    const int t = threadIdx.x, nt = blockDim.x;
+    const int nc = cs.ncert, nd = cs.ndropped;
+    if (t == 0) cs.collapsed = 0;  // published by the first barrier below
+    for (int pass = 0; pass < 2; ++pass) {
+        // G[a][b] = e_C[a]^H w_D[b], four lanes per product
+        for (int e0 = 0; e0 < nc * nd; e0 += nt / 4) {
+            const int e = e0 + (t >> 2), part = t & 3;
             double2 d = make_double2(0, 0);
-            if (k < m && k != jd && cs.cert[k])
+            if (e < nc * nd) {
+                const double2* ec = W + cs.certcols[e / nd] * m;
+                const double2* wd = W + cs.dropped[e % nd] * m;
                 for (int i = part; i < m; i += 4) {
-                    const double2 a = W[k * m + i], b = W[jd * m + i];
+                    const double2 a = ec[i], b = wd[i];
                     d.x = fma(a.x, b.x, fma(a.y, b.y, d.x));
                     d.y = fma(a.x, b.y, fma(-a.y, b.x, d.y));
                 }
+            }
             d.x += __shfl_xor_sync(0xffffffffu, d.x, 1);
             d.y += __shfl_xor_sync(0xffffffffu, d.y, 1);
             d.x += __shfl_xor_sync(0xffffffffu, d.x, 2);
             d.y += __shfl_xor_sync(0xffffffffu, d.y, 2);
-            if (k < m && part == 0) cs.dots[k] = (k != jd && cs.cert[k]) ? d : make_double2(0, 0);
-            __syncthreads();
-            // row i = k: w_jd[i] -= sum_kk dots[kk] e_kk[i]
-            double2 acc = make_double2(0, 0);
-            if (k < m)
-                for (int kk = part; kk < m; kk += 4) {
-                    const double2 dk = cs.dots[kk], e = W[kk * m + k];
-                    acc.x = fma(dk.x, e.x, fma(-dk.y, e.y, acc.x));
-                    acc.y = fma(dk.x, e.y, fma(dk.y, e.x, acc.y));
-                }
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-            __syncthreads();
-            if (k < m && part == 0) W[jd * m + k] = csub(W[jd * m + k], acc);
-            __syncthreads();
-        }
-        if (t < kWarp) {
-            double v = 0;
-            for (int i = t; i < m; i += kWarp) v += cnorm(W[jd * m + i]);
-            v = group_sum<kWarp>(v);
-            if (t == 0) cs.nrm1 = sqrt(v);
+            if (e < nc * nd && (t & 3) == 0) G[e] = d;
         }
         __syncthreads();
-        const double nrm = cs.nrm1;
-        if (!(nrm > 1e-6)) {  // collapsed: leave this bin to the generic kernel
-            if (t == 0) cs.eligible = 0;
-            __syncthreads();
-            return;
+        // w_D[b][i] -= sum_a G[a][b] e_C[a][i]
+        for (int o = t; o < nd * m; o += nt) {
+            const int b = o / m, i = o % m;
+            double2 acc = make_double2(0, 0);
+            for (int a = 0; a < nc; ++a) {
+                const double2 g = G[a * nd + b], ev = W[cs.certcols[a] * m + i];
+                acc.x = fma(g.x, ev.x, fma(-g.y, ev.y, acc.x));
+                acc.y = fma(g.x, ev.y, fma(g.y, ev.x, acc.y));
+            }
+            double2* w = W + cs.dropped[b] * m + i;
+            *w = csub(*w, acc);
         }
-        if (t < m) W[jd * m + t] = cscale(1.0 / nrm, W[jd * m + t]);
-        if (t == 0) cs.cert[jd] = 1;
+        __syncthreads();
+    }
+    // D <- D L^-H with D^H D = L L^H (CholeskyQR, twice): the Q factor of D
+    // in rank order, i.e. the Gram-Schmidt result; L_jj is the norm of column
+    // j after projection against the earlier ones (collapse test).
+    double* invd = cs.invd;
+    for (int pass = 0; pass < 2; ++pass) {
+        // packed lower Gram G[i(i+1)/2 + k] = d_i^H d_k, k <= i
+        const int np = nd * (nd + 1) / 2;
+        for (int e0 = 0; e0 < np; e0 += nt / 4) {
+            const int e = e0 + (t >> 2), part = t & 3;
+            double2 d = make_double2(0, 0);
+            if (e < np) {
+                int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+                while (i * (i + 1) / 2 > e) --i;
+                while ((i + 1) * (i + 2) / 2 <= e) ++i;
+                const int k = e - i * (i + 1) / 2;
+                const double2* di = W + cs.dropped[i] * m;
+                const double2* dk = W + cs.dropped[k] * m;
+                for (int r = part; r < m; r += 4) {
+                    const double2 a = di[r], b = dk[r];
+                    d.x = fma(a.x, b.x, fma(a.y, b.y, d.x));
+                    d.y = fma(a.x, b.y, fma(-a.y, b.x, d.y));
+                }
+            }
+            d.x += __shfl_xor_sync(0xffffffffu, d.x, 1);
+            d.y += __shfl_xor_sync(0xffffffffu, d.y, 1);
+            d.x += __shfl_xor_sync(0xffffffffu, d.x, 2);
+            d.y += __shfl_xor_sync(0xffffffffu, d.y, 2);
+            if (e < np && (t & 3) == 0) G[e] = d;
+        }
+        __syncthreads();
+        if (t < kWarp) {  // right-looking Cholesky, one warp
+            for (int j = 0; j < nd; ++j) {
+                const double gjj = G[j * (j + 1) / 2 + j].x;
+                if (!(gjj > 1e-12)) {  // projected norm <= 1e-6: collapsed
+                    if (t == 0) {
+                        cs.eligible = 0;
+                        cs.collapsed = 1;
+                    }
+                    break;
+                }
+                const double ljj = sqrt(gjj), inv = 1.0 / ljj;
+                for (int i = j + 1 + t; i < nd; i += kWarp) {
+                    double2& gij = G[i * (i + 1) / 2 + j];
+                    gij = cscale(inv, gij);
+                }
+                __syncwarp();
+                for (int i = j + 1 + t; i < nd; i += kWarp) {
+                    const double2 lij = G[i * (i + 1) / 2 + j];
+                    for (int k = j + 1; k <= i; ++k) {
+                        const double2 lkj = G[k * (k + 1) / 2 + j];
+                        double2& gik = G[i * (i + 1) / 2 + k];
+                        gik.x -= fma(lij.x, lkj.x, lij.y * lkj.y);
+                        gik.y -= fma(lij.y, lkj.x, -lij.x * lkj.y);
+                    }
+                }
+                if (t == 0) invd[j] = inv;
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (cs.collapsed) return;  // uniform: written before the barrier above
+        // row solve q_rb = (d_rb - sum_{a<b} q_ra conj(L_ba)) / L_bb, four lanes per row
+        {
+            const int r = t >> 2, part = t & 3;
+            const unsigned gm = 0xfu << ((t & 31) & ~3);
+            if (r < m) {
+                for (int b = 0; b < nd; ++b) {
+                    double2 acc = make_double2(0, 0);
+                    const double2* lb = G + b * (b + 1) / 2;
+                    for (int a = part; a < b; a += 4) {
+                        const double2 q = W[cs.dropped[a] * m + r], l = lb[a];
+                        acc.x = fma(q.x, l.x, fma(q.y, l.y, acc.x));
+                        acc.y = fma(q.y, l.x, fma(-q.x, l.y, acc.y));
+                    }
+                    acc.x += __shfl_xor_sync(gm, acc.x, 1);
+                    acc.y += __shfl_xor_sync(gm, acc.y, 1);
+                    acc.x += __shfl_xor_sync(gm, acc.x, 2);
+                    acc.y += __shfl_xor_sync(gm, acc.y, 2);
+                    if (part == 0) {
+                        double2* w = W + cs.dropped[b] * m + r;
+                        *w = cscale(invd[b], csub(*w, acc));
+                    }
+                    __syncwarp(gm);
+                }
+            }
+        }
         __syncthreads();
     }
 }
@@ -227,70 +307,88 @@ __device__ void apply_span(double2* W, int m, int d, CanonScratch& cs) {
 // ---------------------------------------------------------------------------
 
 struct QrScratch {
-    double nrm2[kMaxM];
-    int piv[kMaxM];  // column k of A P is column piv[k] of A
-    double2 u0, beta;
+    double2 u[kMaxM];       // Householder vector of the current step (zero above k)
+    unsigned key[kMaxM];    // pivot key per physical column (0: already pivoted)
+    int piv[kMaxM];         // column k of A P is column piv[k] of A
     double tau;
-    int p;
 };
 
+// Pivot key: the remaining squared norm as float bits (monotonic for x >= 0)
+// with the low 6 bits replaced by 63 - column, so one unsigned max picks the
+// largest norm (to 2^-17 relative) and the lowest column among equals.
+__device__ __forceinline__ unsigned pivot_key(double n2, int c) {
+    const float f = __double2float_rz(fmin(n2, 1e38));
+    return ((__float_as_uint(f) & ~63u) | (unsigned)(63 - c)) + 1u;
+}
+
+// sqrt for positive normal FP64 values (x * rsqrt(x), Newton-refined)
+__device__ __forceinline__ double fast_sqrt(double x) { return x > 0 ? x * fast_rsqrt(x) : 0.0; }
+
+#ifdef SSLG_QR_TIMING  // development harness only (tools/ubench/qr.cu)
+__device__ long long g_qr_clk[8];
+#define QR_T(i) do { if (threadIdx.x == SSLG_QR_TIMING) { long long _n = clock64(); g_qr_clk[i] += _n - _t; _t = _n; } } while (0)
+#else
+#define QR_T(i) do { } while (0)
+#endif
+
+// Column-resident QRCP: 4 lanes own one physical column of A in registers
+// (rows l, l+4, ...), so a step moves only the Householder vector through
+// shared memory.  Per step: every warp reduces the pivot keys with one
+// redux.max; the pivot's group forms the reflector H = I - tau u u^H
+// (H x = beta e_k) from the exact norm of its rows >= k that it computed in
+// the previous step; one barrier; every other unpivoted group applies H to
+// its column and accumulates the exact norm of its rows > k in the same pass;
+// one barrier.  The pivot section is kept to a few dozen instructions: it is
+// the serial part of every step.
+template <int MC>
 __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
-    const int t = threadIdx.x, warp = t / kWarp, lane = t % kWarp;
-    constexpr int kWarps = kJacThreads / kWarp;
-    for (int j = warp; j < m; j += kWarps) {
-        double v = 0;
-        for (int i = lane; i < m; i += kWarp) v += cnorm(W[j * m + i]);
-        v = group_sum<kWarp>(v);
-        if (lane == 0) qs.nrm2[j] = v;
+    constexpr int RP = MC > 0 ? (MC + 3) / 4 : kMaxM / 4;
+#ifdef SSLG_QR_TIMING
+    long long _t = clock64();
+#endif
+    const int t = threadIdx.x, c = t >> 2, l = t & 3, lane = t & 31;
+    const bool own = c < m;
+    const unsigned gmask = 0xfu << (lane & ~3);
+    double2 y[RP];
+#pragma unroll
+    for (int v = 0; v < RP; ++v) {
+        const int i = l + 4 * v;
+        y[v] = (own && i < m) ? W[c * m + i] : make_double2(0, 0);
     }
-    if (t < m) qs.piv[t] = t;
+    double nrm;  // exact squared norm of rows >= k (rows > k - 1 after the previous update)
+    {
+        double a0 = 0, a1 = 0;
+#pragma unroll
+        for (int v = 0; v < RP; v += 2) a0 = fma(y[v].x, y[v].x, fma(y[v].y, y[v].y, a0));
+#pragma unroll
+        for (int v = 1; v < RP; v += 2) a1 = fma(y[v].x, y[v].x, fma(y[v].y, y[v].y, a1));
+        nrm = a0 + a1;
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+        if (own && l == 0) qs.key[c] = pivot_key(nrm, c);
+        if (t < kMaxM) {
+            qs.u[t] = make_double2(0, 0);
+            if (t >= m) qs.key[t] = 0u;
+        }
+    }
+    int mypos = -1;
+    double2 mybeta = make_double2(0, 0);
     __syncthreads();
     for (int k = 0; k < m; ++k) {
-        // warp 0 alone: pivot (first column of largest remaining norm), column
-        // swap, and the reflector H = I - tau u u^H with H x = beta e_k
-        if (warp == 0) {
-            double best = -1;
-            int bi = k;
-            for (int j = k + lane; j < m; j += kWarp)
-                if (qs.nrm2[j] > best) {
-                    best = qs.nrm2[j];
-                    bi = j;
-                }
+        const unsigned kk = __reduce_max_sync(0xffffffffu, max(qs.key[lane], qs.key[lane + 32]));
+        const int p = 63 - (int)((kk - 1u) & 63u);
+        QR_T(0);
+        if (c == p) {
+            double2 x0 = make_double2(0, 0);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) {
-                    best = ob;
-                    bi = oi;
-                }
+            for (int v = 0; v < RP; ++v) {
+                const int i = l + 4 * v;
+                if (i == k) x0 = y[v];
+                if (i >= k && i < m) qs.u[i] = y[v];
             }
-            const int p = bi;
-            double a2 = 0;
-            for (int i = lane; i < m; i += kWarp) {
-                double2 xk = W[k * m + i];
-                if (p != k) {
-                    const double2 xp = W[p * m + i];
-                    W[p * m + i] = xk;
-                    W[k * m + i] = xp;
-                    xk = xp;
-                }
-                if (i >= k) a2 = fma(xk.x, xk.x, fma(xk.y, xk.y, a2));
-            }
-            a2 = group_sum<kWarp>(a2);
-            __syncwarp();
-            if (lane == 0) {
-                if (p != k) {
-                    const double x = qs.nrm2[k];
-                    qs.nrm2[k] = qs.nrm2[p];
-                    qs.nrm2[p] = x;
-                    const int i = qs.piv[k];
-                    qs.piv[k] = qs.piv[p];
-                    qs.piv[p] = i;
-                }
-                const double2 x0 = W[k * m + k];
-                const double alpha = sqrt(a2);
+            if (l == (k & 3)) {  // the lane that owns row k finishes the reflector
                 const double ax2 = fma(x0.x, x0.x, x0.y * x0.y);
+                const double alpha = fast_sqrt(nrm);
                 double2 ph = make_double2(1.0, 0.0);
                 double ax0 = 0.0;
                 if (ax2 > 0) {
@@ -298,58 +396,113 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
                     ax0 = ax2 * ri;
                     ph = make_double2(x0.x * ri, x0.y * ri);
                 }
-                qs.beta = make_double2(-ph.x * alpha, -ph.y * alpha);
-                qs.u0 = make_double2(x0.x + ph.x * alpha, x0.y + ph.y * alpha);
+                mybeta = make_double2(-ph.x * alpha, -ph.y * alpha);
+                qs.u[k] = make_double2(x0.x + ph.x * alpha, x0.y + ph.y * alpha);
                 qs.tau = alpha > 0 ? fast_rcp(alpha * (alpha + ax0)) : 0.0;
+                qs.key[p] = 0u;
+                qs.piv[k] = p;
             }
+            mypos = k;
         }
+        QR_T(1);
         __syncthreads();
-        const double tau = qs.tau;
-        const double2 u0 = qs.u0;
-        if (tau != 0.0) {  // trailing columns, 4 lanes per column, all in parallel
-            const int j = k + 1 + (t >> 2), part = t & 3;
-            double2 sdot = make_double2(0, 0);
-            if (j < m)
-                for (int i = k + 1 + part; i < m; i += 4) {
-                    const double2 u = W[k * m + i], y = W[j * m + i];
-                    sdot.x = fma(u.x, y.x, fma(u.y, y.y, sdot.x));
-                    sdot.y = fma(u.x, y.y, fma(-u.y, y.x, sdot.y));
-                }
-            sdot.x += __shfl_xor_sync(0xffffffffu, sdot.x, 1);
-            sdot.y += __shfl_xor_sync(0xffffffffu, sdot.y, 1);
-            sdot.x += __shfl_xor_sync(0xffffffffu, sdot.x, 2);
-            sdot.y += __shfl_xor_sync(0xffffffffu, sdot.y, 2);
-            if (j < m) {
-                const double2 yk = W[j * m + k];
-                sdot.x = fma(u0.x, yk.x, fma(u0.y, yk.y, sdot.x));
-                sdot.y = fma(u0.x, yk.y, fma(-u0.y, yk.x, sdot.y));
-                const double2 f = cscale(tau, sdot);
-                for (int i = k + 1 + part; i < m; i += 4) W[j * m + i] = csub(W[j * m + i], cmul(f, W[k * m + i]));
-            }
-            __syncwarp();  // every lane of the group has read y_k
-            if (j < m) {
-                const double2 yk = W[j * m + k];
-                const double2 f = cscale(tau, sdot);
-                if (part == 0) {
-                    const double2 nk = csub(yk, cmul(f, u0));
-                    W[j * m + k] = nk;
-                    qs.nrm2[j] = fmax(0.0, qs.nrm2[j] - cnorm(nk));
-                }
-            }
-        }
-        __syncthreads();
-        if (t == 0) W[k * m + k] = qs.beta;
+        QR_T(2);
+        {  // every group runs the update (no divergence around the group
+           // shuffles); pivoted and padding groups apply a zero multiple
+            const bool act = own && mypos < 0;
+            const double tau = act ? qs.tau : 0.0;
+            // rows above k have u = 0: enter the unrolled row chunks at the
+            // first active one (warp-uniform jump, no predicated-off issue)
+            const int v0 = k >> 2;
+            double sx0 = 0, sy0 = 0, sx1 = 0, sy1 = 0;
+#define QR_DOT(v)                                                          \
+    if ((v) < RP) {                                                        \
+        const double2 u = qs.u[l + 4 * (v)];                               \
+        if ((v) & 1) {                                                     \
+            sx1 = fma(u.x, y[v].x, fma(u.y, y[v].y, sx1));                 \
+            sy1 = fma(u.x, y[v].y, fma(-u.y, y[v].x, sy1));                \
+        } else {                                                           \
+            sx0 = fma(u.x, y[v].x, fma(u.y, y[v].y, sx0));                 \
+            sy0 = fma(u.x, y[v].y, fma(-u.y, y[v].x, sy0));                \
+        }                                                                  \
     }
-    __syncthreads();
-    // X = R^H: column j of X is the conjugated row j of R (lower triangular)
-    for (int e = t; e < m * m; e += blockDim.x) {
-        const int j = e / m, i = e % m;  // X column j, row i
-        if (i > j) {
-            const double2 rji = W[i * m + j];
-            W[j * m + i] = cconj(rji);
-            W[i * m + j] = make_double2(0, 0);
-        } else if (i == j) {
-            W[e] = cconj(W[e]);
+            switch (v0) {
+                case 0: QR_DOT(0) [[fallthrough]];
+                case 1: QR_DOT(1) [[fallthrough]];
+                case 2: QR_DOT(2) [[fallthrough]];
+                case 3: QR_DOT(3) [[fallthrough]];
+                case 4: QR_DOT(4) [[fallthrough]];
+                case 5: QR_DOT(5) [[fallthrough]];
+                case 6: QR_DOT(6) [[fallthrough]];
+                case 7: QR_DOT(7) [[fallthrough]];
+                case 8: QR_DOT(8) [[fallthrough]];
+                case 9: QR_DOT(9) [[fallthrough]];
+                case 10: QR_DOT(10) [[fallthrough]];
+                case 11: QR_DOT(11) [[fallthrough]];
+                case 12: QR_DOT(12) [[fallthrough]];
+                case 13: QR_DOT(13) [[fallthrough]];
+                case 14: QR_DOT(14) [[fallthrough]];
+                default: QR_DOT(15)
+            }
+#undef QR_DOT
+            double sx = sx0 + sx1, sy = sy0 + sy1;
+            sx += __shfl_xor_sync(gmask, sx, 1);
+            sy += __shfl_xor_sync(gmask, sy, 1);
+            sx += __shfl_xor_sync(gmask, sx, 2);
+            sy += __shfl_xor_sync(gmask, sy, 2);
+            const double fx = tau * sx, fy = tau * sy;
+            double a0 = 0, a1 = 0;
+#define QR_UPD(v)                                                          \
+    if ((v) < RP) {                                                        \
+        const double2 u = qs.u[l + 4 * (v)];                               \
+        y[v].x -= fx * u.x - fy * u.y;                                     \
+        y[v].y -= fx * u.y + fy * u.x;                                     \
+        const double e = (l + 4 * (v) > k) ? fma(y[v].x, y[v].x, y[v].y * y[v].y) : 0.0; \
+        if ((v) & 1) a1 += e;                                              \
+        else a0 += e;                                                      \
+    }
+            switch (v0) {
+                case 0: QR_UPD(0) [[fallthrough]];
+                case 1: QR_UPD(1) [[fallthrough]];
+                case 2: QR_UPD(2) [[fallthrough]];
+                case 3: QR_UPD(3) [[fallthrough]];
+                case 4: QR_UPD(4) [[fallthrough]];
+                case 5: QR_UPD(5) [[fallthrough]];
+                case 6: QR_UPD(6) [[fallthrough]];
+                case 7: QR_UPD(7) [[fallthrough]];
+                case 8: QR_UPD(8) [[fallthrough]];
+                case 9: QR_UPD(9) [[fallthrough]];
+                case 10: QR_UPD(10) [[fallthrough]];
+                case 11: QR_UPD(11) [[fallthrough]];
+                case 12: QR_UPD(12) [[fallthrough]];
+                case 13: QR_UPD(13) [[fallthrough]];
+                case 14: QR_UPD(14) [[fallthrough]];
+                default: QR_UPD(15)
+            }
+#undef QR_UPD
+            nrm = a0 + a1;
+            nrm += __shfl_xor_sync(gmask, nrm, 1);
+            nrm += __shfl_xor_sync(gmask, nrm, 2);
+            if (act && l == 0) qs.key[c] = pivot_key(nrm, c);
+        }
+        QR_T(3);
+#ifdef SSLG_QR_TIMING
+        if (threadIdx.x == SSLG_QR_TIMING) { g_qr_clk[5] = mypos; g_qr_clk[6] += (own && mypos < 0); }
+#endif
+        __syncthreads();
+        QR_T(4);
+        if (c == p && l == (k & 3)) qs.u[k] = make_double2(0, 0);  // keep u zero above the next step
+    }
+    // X = R^H: the group at pivot position j holds row j of X (conjugated
+    // column j of R: rows < j in registers, beta on the diagonal); X is
+    // lower triangular
+    const int bsrc = (lane & ~3) | (mypos & 3);
+    const double2 bj = make_double2(__shfl_sync(0xffffffffu, mybeta.x, bsrc), __shfl_sync(0xffffffffu, mybeta.y, bsrc));
+    if (own) {
+#pragma unroll
+        for (int v = 0; v < RP; ++v) {
+            const int r = l + 4 * v;
+            if (r < m) W[r * m + mypos] = r < mypos ? cconj(y[v]) : (r == mypos ? cconj(bj) : make_double2(0, 0));
         }
     }
     __syncthreads();
@@ -403,6 +556,62 @@ __device__ void back_multiply(double2* W, const double2* __restrict__ ag, int m,
     }
 }
 
+// Rotation of one pair (gsvd.cpp:642-672) in closed form.  With D = cq - cp,
+// M = |a_pq|^2 and q = sqrt(4M + D^2), the reference's
+//   tau = D / (2|a_pq|), t = sgn(tau) / (|tau| + sqrt(1 + tau^2)),
+//   c = 1 / sqrt(1 + t^2), s = t c
+// are c = sqrt((q + |D|) / (2q)) and s = sgn(D) sqrt(2M / (q (q + |D|))):
+// two dependent rsqrt instead of four.
+struct JRot {
+    double c, sn, alx, aly, bex, bey, cs2;
+    bool on;
+};
+
+__device__ __forceinline__ JRot jrot(double dx, double dy, double cp, double cq) {
+    JRot r;
+    r.on = true;
+    const double M = fma(dx, dx, dy * dy);
+    const double D = cq - cp;
+    const double aD = fabs(D);
+    const double iM = fast_rsqrt(M);  // 1 / |a_pq|
+    const double phx = dx * iM, phy = dy * iM;
+    double c, sn;
+    if (__builtin_expect(aD < 1e150 && M < 1e300, 1)) {
+        const double q2 = fma(D, D, 4.0 * M);
+        const double q = q2 * fast_rsqrt(q2);
+        const double iv = fast_rsqrt(q * (q + aD));
+        c = (q + aD) * iv * 0.70710678118654752440;
+        sn = copysign(1.41421356237309504880 * (M * iM) * iv, D);
+    } else {  // tau^2 would overflow: the reference's formula, t ~ 1 / (2|tau|)
+        const double tau = D * (0.5 * iM);
+        const double t = copysign(0.5 / fabs(tau), tau);
+        c = fast_rsqrt(fma(t, t, 1.0));
+        sn = t * c;
+    }
+    r.c = c;
+    r.sn = sn;
+    r.alx = sn * phx;
+    r.aly = -sn * phy;
+    r.bex = c * phx;
+    r.bey = -c * phy;
+    r.cs2 = 2.0 * c * sn * (M * iM);
+    return r;
+}
+template <int RPL>
+__device__ __forceinline__ void japply(double2 (&P)[RPL], double2 (&Q)[RPL], const JRot& r, double& cp, double& cq) {
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+        const double2 x = P[u], y = Q[u];
+        P[u].x = fma(r.c, x.x, fma(-r.alx, y.x, r.aly * y.y));
+        P[u].y = fma(r.c, x.y, fma(-r.alx, y.y, -r.aly * y.x));
+        Q[u].x = fma(r.sn, x.x, fma(r.bex, y.x, -r.bey * y.y));
+        Q[u].y = fma(r.sn, x.y, fma(r.bex, y.y, r.bey * y.x));
+    }
+    const double np = r.c * r.c * cp - r.cs2 + r.sn * r.sn * cq;
+    cq = r.sn * r.sn * cp + r.cs2 + r.c * r.c * cq;
+    cp = np;
+}
+
 // One Jacobi pair in registers (gsvd.cpp:642-672): P is the lower-index
 // column.  Returns whether a rotation was applied.
 template <int R, int L>
@@ -424,35 +633,7 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
     const double2 dot = group_sum2<L>(make_double2(d0x + d1x, d0y + d1y));
     const double mag2 = fma(dot.x, dot.x, dot.y * dot.y);
     if (cp <= drop || cq <= drop || mag2 <= 1e-28 * cp * cq) return false;
-    // t = sign(tau) / (|tau| + sqrt(1 + tau^2)), tau = (cq - cp) / (2 |apq|)
-    const double inv_mag = fast_rsqrt(mag2);
-    const double mag = mag2 * inv_mag;
-    const double phx = dot.x * inv_mag, phy = dot.y * inv_mag;
-    const double tau = (cq - cp) * (0.5 * inv_mag);
-    const double atau = fabs(tau);
-    double t;
-    if (atau < 1e150) {
-        const double tt = fma(tau, tau, 1.0);
-        t = copysign(fast_rcp(atau + tt * fast_rsqrt(tt)), tau);
-    } else {  // tau^2 would overflow: t = 1 / (2 |tau|)
-        t = copysign(0.5 / atau, tau);
-    }
-    const double c = fast_rsqrt(fma(t, t, 1.0));
-    const double sn = t * c;
-    const double alx = sn * phx, aly = -sn * phy;  // s * conj(ph)
-    const double bex = c * phx, bey = -c * phy;    // c * conj(ph)
-#pragma unroll
-    for (int u = 0; u < R; ++u) {
-        const double2 x = P[u], y = Q[u];
-        P[u].x = fma(c, x.x, fma(-alx, y.x, aly * y.y));
-        P[u].y = fma(c, x.y, fma(-alx, y.y, -aly * y.x));
-        Q[u].x = fma(sn, x.x, fma(bex, y.x, -bey * y.y));
-        Q[u].y = fma(sn, x.y, fma(bex, y.y, bey * y.x));
-    }
-    const double cs2 = 2.0 * c * sn * mag;
-    const double np = c * c * cp - cs2 + sn * sn * cq;
-    cq = sn * sn * cp + cs2 + c * c * cq;
-    cp = np;
+    japply<R>(P, Q, jrot(dot.x, dot.y, cp, cq), cp, cq);
     return true;
 }
 
@@ -543,7 +724,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     double2* ag = precond ? a.ascratch + (size_t)blk * m * m : nullptr;
     if (precond) {
         for (int e = tid; e < m * m; e += blockDim.x) ag[e] = W[e];
-        qrcp_to_rh(W, m, qs);
+        qrcp_to_rh<MC>(W, m, qs);
     }
     mark(1);
 
@@ -708,25 +889,27 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         // orthonormal basis below.
         // In the preconditioned path u_j = A P x_j / sigma_j carries the
         // Jacobi's residual coupling to larger-sigma vectors amplified by
-        // sigma_k / sigma_j; every vector below 1e-4 sigma_max (and the whole
-        // vanishing block) is therefore re-orthonormalized, in rank order,
-        // against all larger ones — which removes exactly those components
-        // (the ones above keep an error <= 1e4 x the Jacobi tolerance).
+        // sigma_k / sigma_j; every vector below kReorth sigma_max (and the
+        // whole vanishing block) is therefore re-orthonormalized, in rank
+        // order, against all larger ones — which removes exactly those
+        // components (the ones above keep an error <= 1/kReorth x the
+        // Jacobi's 1e-14 relative orthogonality, i.e. <= 1e-9).
         int r0 = lead_end;
         if (precond)
             for (int rk = 0; rk < lead_end; ++rk)
-                if (s_sig[s_perm[rk]] < 1e-4 * smax) {
+                if (s_sig[s_perm[rk]] < kReorth * smax) {
                     r0 = rk;
                     break;
                 }
-        int nd = 0;
+        int nd = 0, nc = 0;
         for (int rk = 0; rk < m; ++rk) {
             const int j = s_perm[rk];
             const bool dropped = precond ? (rk >= r0) : !(cn[j] > s_drop);
-            cs.cert[j] = dropped ? 0 : 1;
             if (dropped) cs.dropped[nd++] = j;
+            else cs.certcols[nc++] = j;
         }
         cs.ndropped = nd;
+        cs.ncert = nc;
         const bool clean = converged;
         cs.ngroups = ng;
         cs.nvanish = z;
@@ -735,7 +918,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     __syncthreads();
     // the preconditioned vectors are re-orthonormalized whichever kernel
     // canonicalizes them (the generic one reads the lead vectors too)
-    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis(W, m, cs);
+    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis(W, Y, m, cs);
     mark(4);
     const bool fused = cs.eligible;
     if (a.canonical && fused) {
@@ -746,6 +929,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
             pick_in_span(W, Y, m, z, true, cs);
             apply_span(W, m, z, cs);
         }
+        mark(7);
         for (int gi = 0; gi < cs.ngroups; ++gi) {
             const int i0 = cs.groups[gi][0];
             const int d = cs.groups[gi][1] - i0 + 1;
@@ -810,7 +994,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     }
 }
 
-size_t jacobi_smem_bytes(int m) { return (size_t)m * m * sizeof(double2) + (size_t)kMaxM * kYld * sizeof(double2); }
+size_t jacobi_smem_bytes(int m) { return (size_t)m * m * sizeof(double2) + (size_t)kScratch * sizeof(double2); }
 
 void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
     const size_t smem = jacobi_smem_bytes(a.m);
