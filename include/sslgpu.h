@@ -112,7 +112,8 @@ int sslg_build_topology(const double* dirs_deg, uint32_t n, double radius_deg, u
 /* ---- streaming hot path (run_locate's per-frame loop, pipeline.cpp:227-245) */
 
 /* Estimates of one emitted block.  Mirrors FrameEstimates + SourceEstimate
- * (pipeline.hpp:63-66, music.hpp:88-93); arrays hold num_sources slots. */
+ * (pipeline.hpp:63-66, music.hpp:88-93); arrays hold num_sources slots, the
+ * first `count` valid (unused slots: index 0xffffffff, power 0, low 0). */
 typedef struct sslg_block_out {
     uint32_t frame_index; /* frame that completed the block */
     uint32_t count;       /* estimates written (<= num_sources) */
@@ -148,6 +149,46 @@ int sslg_integrate_peaks_device(sslg_ctx* ctx, const void* p_dev, uint32_t n, ui
 int sslg_reset_window(sslg_ctx* ctx);
 /* Blocks until the context stream is idle. */
 int sslg_synchronize(sslg_ctx* ctx);
+
+/* ---- STFT front end: SampleBlock in (run_locate, pipeline.cpp:210-247) --- */
+
+/* StftConfig (types.hpp:41-52). window: 0 hann (periodic), 1 rectangular. */
+typedef struct sslg_stft_config {
+    uint32_t frame_length; /* power of two, <= 8192 on the device */
+    uint32_t shift;
+    int window;
+    uint32_t bin_min, bin_max; /* inclusive; bin_max - bin_min + 1 == sslg_config.bins */
+} sslg_stft_config;
+
+/* StftConfig defaults: 512 / 160 / hann / 16..88 (types.hpp:43-52). */
+void sslg_stft_config_default(sslg_stft_config* s);
+/* Validates like StftConfig::validate (stft.cpp:9-16), builds make_window
+ * (stft.cpp:28-36) and the fft_pow2 twiddles (fft.hpp:29-38) and sizes the
+ * device sample history.  Frames are bit-identical to stft_frame. */
+int sslg_set_stft(sslg_ctx* ctx, const sslg_stft_config* s);
+/* stft_stream over one SampleBlock (stft.cpp:61-68): pcm [m][nsamples] f32
+ * channel-major (SampleBlock::channels); frames [nframes][m][bins] cf32 with
+ * nframes = stft_frame_count (stft.cpp:38-42), at most cap_frames (pass
+ * frames == NULL to query *nframes).  Does not touch the correlation window. */
+int sslg_stft(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, float* frames, uint32_t cap_frames,
+              uint32_t* nframes);
+/* Frames and result blocks the next sslg_push_samples of nsamples samples
+ * per channel will produce (sizing aid for the result arrays). */
+int sslg_samples_pending(const sslg_ctx* ctx, uint64_t nsamples, uint32_t* frames, uint32_t* blocks);
+/* Streaming run_locate: appends pcm [m][nsamples] to the context's sample
+ * history (frames continue across calls at multiples of shift), transforms
+ * every complete frame on the device straight into the correlation window
+ * and runs the hot path as sslg_push_frames.  Result arrays hold cap_blocks
+ * blocks; SSLG_VALIDATION if the push would emit more. */
+int sslg_push_samples(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint32_t cap_blocks,
+                      sslg_block_out* blocks, uint32_t* est_idx, double* est_power, uint8_t* est_low, double* power,
+                      uint32_t* emitted);
+/* run_locate (pipeline.cpp:210-247): a fresh correlation window and sample
+ * history, then sslg_push_samples over the whole SampleBlock; frame indices
+ * count from the block's first frame. */
+int sslg_locate_samples(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint32_t cap_blocks,
+                        sslg_block_out* blocks, uint32_t* est_idx, double* est_power, uint8_t* est_low,
+                        double* power, uint32_t* emitted);
 
 /* ---- stage entry points (host buffers, one call per reference function) */
 

@@ -457,6 +457,18 @@ class _Port:
                                          C.c_uint32(rebuild_interval), _p(out, _f32p), C.byref(n)))
         return out[: n.value]
 
+    def stft(self, pcm, frame_length=512, shift=160, window=0, bin_min=16, bin_max=88):
+        """stft_stream (stft.cpp:38-68, fft.hpp:15-68): pcm [m][n] -> [F][m][bins] complex64."""
+        pcm = np.ascontiguousarray(pcm, np.float32)
+        m, n = pcm.shape
+        nf = C.c_uint32()
+        args = (C.c_uint32(m), C.c_uint64(n), C.c_uint32(frame_length), C.c_uint32(shift), C.c_int(window),
+                C.c_uint32(bin_min), C.c_uint32(bin_max))
+        self._chk(self.L.orc_stft(_p(pcm, _f32p), *args, None, C.byref(nf)))
+        out = np.zeros((nf.value, m, bin_max - bin_min + 1), np.complex64)
+        self._chk(self.L.orc_stft(_p(pcm, _f32p), *args, _p(out, _f32p), C.byref(nf)))
+        return out
+
     def mat_inverse(self, k, pivoting=1, bin_label=0):
         k = np.ascontiguousarray(k, np.complex64)
         out = np.zeros(k.shape, np.complex128)

@@ -696,3 +696,84 @@ int orc_peaks(const double* power, uint32_t n, const uint32_t* offsets, const ui
     free(peaks);
     return 0;
 }
+
+/* ------------------------------------------------------------------------- */
+/* STFT front end                                                            */
+/* ------------------------------------------------------------------------- */
+
+/* make_window (stft.cpp:28-36): periodic Hann evaluated in double, rounded
+ * to float once. */
+void orc_window(int kind, uint32_t length, float* w) {
+    for (uint32_t n = 0; n < length; ++n)
+        w[n] = kind == 0 ? (float)(0.5 - 0.5 * cos(2.0 * M_PI * (double)n / (double)length)) : 1.0f;
+}
+
+/* fft_pow2<float> (fft.hpp:15-44): bit-reversal permutation, then radix-2
+ * stages with the twiddle advanced by w *= wlen (complex<double>, textbook
+ * product under -fcx-limited-range), butterflies in double, results rounded
+ * to float after every stage. */
+static void fft_pow2_f(float* re, float* im, uint32_t n) {
+    for (uint32_t i = 1, j = 0; i < n; ++i) {
+        uint32_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) {
+            float t = re[i]; re[i] = re[j]; re[j] = t;
+            t = im[i]; im[i] = im[j]; im[j] = t;
+        }
+    }
+    for (uint32_t len = 2; len <= n; len <<= 1) {
+        const double ang = -2.0 * M_PI / (double)len;
+        const cd wlen = c_make(cos(ang), sin(ang));
+        for (uint32_t i = 0; i < n; i += len) {
+            cd w = c_make(1.0, 0.0);
+            for (uint32_t k = 0; k < len / 2; ++k) {
+                const cd u = c_make(re[i + k], im[i + k]);
+                const cd v = c_mul(c_make(re[i + k + len / 2], im[i + k + len / 2]), w);
+                re[i + k] = (float)(u.re + v.re);
+                im[i + k] = (float)(u.im + v.im);
+                re[i + k + len / 2] = (float)(u.re - v.re);
+                im[i + k + len / 2] = (float)(u.im - v.im);
+                w = c_mul(w, wlen);
+            }
+        }
+    }
+}
+
+int orc_stft(const float* pcm, uint32_t m, uint64_t nsamples, uint32_t frame_length, uint32_t shift, int window,
+             uint32_t bin_min, uint32_t bin_max, float* frames, uint32_t* nframes) {
+    /* StftConfig::validate (stft.cpp:9-16) */
+    if (frame_length == 0) return set_err(2, "frame_length must be positive");
+    if (shift == 0) return set_err(2, "shift must be positive");
+    if (shift > frame_length) return set_err(2, "shift must not exceed frame_length");
+    if (bin_min > bin_max) return set_err(2, "bin_min must not exceed bin_max");
+    if (bin_max > frame_length / 2) return set_err(2, "bin_max exceeds the half spectrum of frame_length");
+    if (frame_length & (frame_length - 1)) return set_err(2, "oracle STFT covers power-of-two lengths only");
+    /* stft_frame_count (stft.cpp:38-42) */
+    const uint64_t nf = nsamples < frame_length ? 0 : (nsamples - frame_length) / shift + 1;
+    if (nframes) *nframes = (uint32_t)nf;
+    if (!frames) return 0;
+    const uint32_t nb = bin_max - bin_min + 1;
+    float* w = (float*)malloc(sizeof(float) * frame_length);
+    float* re = (float*)malloc(sizeof(float) * frame_length);
+    float* im = (float*)malloc(sizeof(float) * frame_length);
+    orc_window(window, frame_length, w);
+    for (uint64_t f = 0; f < nf; ++f)
+        for (uint32_t c = 0; c < m; ++c) {
+            const float* src = pcm + (uint64_t)c * nsamples + f * shift;  /* stft.cpp:49-53 */
+            for (uint32_t i = 0; i < frame_length; ++i) {
+                re[i] = src[i] * w[i];
+                im[i] = 0.0f;
+            }
+            fft_pow2_f(re, im, frame_length);
+            float* dst = frames + ((f * m + c) * (uint64_t)nb) * 2;  /* retained band (stft.cpp:55-56) */
+            for (uint32_t b = 0; b < nb; ++b) {
+                dst[2 * b] = re[bin_min + b];
+                dst[2 * b + 1] = im[bin_min + b];
+            }
+        }
+    free(w);
+    free(re);
+    free(im);
+    return 0;
+}

@@ -56,6 +56,16 @@ int orc_peaks(const double* power, uint32_t n, const uint32_t* offsets, const ui
               uint32_t num_sources, float low_power_ratio, uint32_t* idx, double* pw, uint8_t* low,
               uint32_t* count);
 
+/* make_window (stft.cpp:28-36): w [length] f32; kind 0 hann (periodic), 1 rectangular. */
+void orc_window(int kind, uint32_t length, float* w);
+
+/* stft_stream / stft_frame (stft.cpp:38-68) with real_dft_half / fft_pow2
+ * (fft.hpp:15-68): pcm [m][nsamples] f32 channel-major (SampleBlock::channels);
+ * frames [nframes][m][bin_max-bin_min+1] cf32, nframes = (nsamples-len)/shift+1
+ * (0 if nsamples < len).  Power-of-two lengths only (the fast path). */
+int orc_stft(const float* pcm, uint32_t m, uint64_t nsamples, uint32_t frame_length, uint32_t shift, int window,
+             uint32_t bin_min, uint32_t bin_max, float* frames, uint32_t* nframes);
+
 #ifdef __cplusplus
 }
 #endif

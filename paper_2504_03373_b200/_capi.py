@@ -50,6 +50,13 @@ class Config(C.Structure):
     ]
 
 
+class StftConfig(C.Structure):
+    """sslg_stft_config (include/sslgpu.h; StftConfig, types.hpp:41-52)."""
+
+    _fields_ = [("frame_length", C.c_uint32), ("shift", C.c_uint32), ("window", C.c_int), ("bin_min", C.c_uint32),
+                ("bin_max", C.c_uint32)]
+
+
 class BlockOut(C.Structure):
     _fields_ = [("frame_index", C.c_uint32), ("count", C.c_uint32)]
 
@@ -81,6 +88,14 @@ EXPORTS = {
     "sslg_last_launch_count": (C.c_uint32, [C.c_void_p]),
     "sslg_probe_fp64_tflops": (C.c_int, [C.c_int, _f64p]),
     "sslg_debug_phase_clocks": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
+    "sslg_stft_config_default": (None, [C.POINTER(StftConfig)]),
+    "sslg_set_stft": (C.c_int, [C.c_void_p, C.POINTER(StftConfig)]),
+    "sslg_stft": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, _f32p, C.c_uint32, _u32p]),
+    "sslg_samples_pending": (C.c_int, [C.c_void_p, C.c_uint64, _u32p, _u32p]),
+    "sslg_push_samples": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, C.c_uint32, C.POINTER(BlockOut), _u32p, _f64p,
+                                    _u8p, _f64p, _u32p]),
+    "sslg_locate_samples": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, C.c_uint32, C.POINTER(BlockOut), _u32p,
+                                      _f64p, _u8p, _f64p, _u32p]),
 }
 
 _lib = None

@@ -119,6 +119,16 @@ struct sslg_ctx {
     uint32_t launches = 0;
     cudaEvent_t ev[6] = {};
     bool timed = false;
+    // STFT front end (sslg_set_stft)
+    sslg_stft_config stft{};
+    bool have_stft = false;
+    float* win = nullptr;          // [frame_length]
+    double2* twiddle = nullptr;    // [frame_length - 1]
+    float* samp[2] = {nullptr, nullptr};  // [m][samp_cap] sample history, ping-pong
+    size_t samp_cap = 0;           // frame_length + max_batch * shift
+    size_t samp_fill = 0;          // samples held in samp[samp_cur]
+    int samp_cur = 0;
+    float2* frame_scratch = nullptr;  // [max_batch][m][bins] for the stage entry point
 };
 
 namespace {
@@ -196,6 +206,8 @@ int run_music(sslg_ctx* c, int n) {
     return 0;
 }
 
+int gate_frames(sslg_ctx* c, uint32_t nframes);
+
 // copies nframes frames (src: host or device) into the ring after the
 // current push count, then gates on non-finite values
 int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind kind) {
@@ -209,9 +221,17 @@ int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind
                            kind, c->stream));
         done += run;
     }
+    return gate_frames(c, nframes);
+}
+
+// non-finite gate over the nframes ring slots after the push count
+// (CorrelationWindow::push -> instantaneous_correlation check, correlation.cpp:16-17)
+int gate_frames(sslg_ctx* c, uint32_t nframes) {
+    const sslg_config& g = c->cfg;
+    const size_t fsz = (size_t)g.m * g.bins;
     TRY(reset_flags(c));
     // gate every staged slot (a wrapped range is two spans)
-    done = 0;
+    uint32_t done = 0;
     while (done < nframes) {
         const int slot = (int)((c->pushed + done) % c->cap);
         const uint32_t run = std::min<uint32_t>(nframes - done, (uint32_t)(c->cap - slot));
@@ -362,6 +382,8 @@ void sslg_destroy(sslg_ctx* c) {
                     c->conv,   c->work, c->ascratch, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
                     c->flags};
     for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch})
         if (p) cudaFree(p);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -529,6 +551,7 @@ int sslg_reset_window(sslg_ctx* c) {
     c->pushed = 0;
     c->since = 0;
     c->last_emitted = 0;
+    c->samp_fill = 0;
     return SSLG_OK;
 }
 
@@ -778,6 +801,198 @@ int sslg_debug_phase_clocks(sslg_ctx* c, double* out8, int reset) {
     for (int i = 0; i < 8; ++i) out8[i] = (double)h[i];
     if (reset) CU(cudaMemset(c->phase_clk, 0, sizeof h));
     return SSLG_OK;
+}
+
+// ---- STFT front end ----------------------------------------------------------
+
+void sslg_stft_config_default(sslg_stft_config* s) {
+    s->frame_length = 512;  // StftConfig defaults (types.hpp:43-52)
+    s->shift = 160;
+    s->window = 0;
+    s->bin_min = 16;
+    s->bin_max = 88;
+}
+
+int sslg_set_stft(sslg_ctx* c, const sslg_stft_config* s) {
+    if (!c || !s) return set_err(SSLG_VALIDATION, "null argument");
+    // StftConfig::validate (stft.cpp:9-16)
+    if (s->frame_length == 0) return set_err(SSLG_VALIDATION, "frame_length must be positive");
+    if (s->shift == 0) return set_err(SSLG_VALIDATION, "shift must be positive");
+    if (s->shift > s->frame_length) return set_err(SSLG_VALIDATION, "shift must not exceed frame_length");
+    if (s->bin_min > s->bin_max) return set_err(SSLG_VALIDATION, "bin_min must not exceed bin_max");
+    if (s->bin_max > s->frame_length / 2)
+        return set_err(SSLG_VALIDATION, "bin_max exceeds the half spectrum of frame_length");
+    if (s->window != 0 && s->window != 1) return set_err(SSLG_VALIDATION, "unknown window");
+    if ((s->frame_length & (s->frame_length - 1)) || s->frame_length > 8192)
+        return set_err(SSLG_VALIDATION, "the device STFT takes power-of-two frame lengths up to 8192");
+    if (s->bin_max - s->bin_min + 1 != c->cfg.bins)
+        return set_err(SSLG_VALIDATION, "STFT band does not match the engine's bin count");
+    CU(cudaSetDevice(c->cfg.device));
+    const uint32_t n = s->frame_length;
+    // make_window (stft.cpp:28-36) and the per-stage twiddle recurrence of
+    // fft_pow2 (fft.hpp:29-38), both on the host exactly as the reference
+    // evaluates them (libm cos/sin, textbook complex product, no contraction)
+    std::vector<float> w(n, 1.0f);
+    if (s->window == 0)
+        for (uint32_t i = 0; i < n; ++i) w[i] = float(0.5 - 0.5 * std::cos(2.0 * M_PI * double(i) / double(n)));
+    std::vector<double2> tw(n > 1 ? n - 1 : 1);
+    for (uint32_t len = 2; len <= n; len <<= 1) {
+        const double ang = -2.0 * M_PI / double(len);
+        const double wlr = std::cos(ang), wli = std::sin(ang);
+        double wr = 1.0, wi = 0.0;
+        for (uint32_t k = 0; k < len / 2; ++k) {
+            tw[len / 2 - 1 + k] = make_double2(wr, wi);
+            const volatile double a = wr * wlr, b = wi * wli, e = wr * wli, f = wi * wlr;
+            wr = a - b;
+            wi = e + f;
+        }
+    }
+    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch})
+        if (p) cudaFree(p);
+    c->win = nullptr;
+    c->twiddle = nullptr;
+    c->samp[0] = c->samp[1] = nullptr;
+    c->frame_scratch = nullptr;
+    c->have_stft = false;
+    c->samp_cap = (size_t)n + (size_t)c->cfg.max_batch * s->shift;
+    TRY(dalloc(&c->win, n));
+    TRY(dalloc(&c->twiddle, tw.size()));
+    TRY(dalloc(&c->samp[0], c->samp_cap * c->cfg.m));
+    TRY(dalloc(&c->samp[1], c->samp_cap * c->cfg.m));
+    TRY(dalloc(&c->frame_scratch, (size_t)c->cfg.max_batch * c->cfg.m * c->cfg.bins));
+    CU(cudaMemcpy(c->win, w.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->twiddle, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    c->stft = *s;
+    c->samp_fill = 0;
+    c->samp_cur = 0;
+    c->have_stft = true;
+    return SSLG_OK;
+}
+
+namespace {
+
+int launch_stft_frames(sslg_ctx* c, const float* pcm_dev, size_t pitch, int nframes, float2* out, int cap,
+                       long long slot0) {
+    StftArgs sa{pcm_dev, c->win, c->twiddle, out, pitch, (int)c->cfg.m, (int)c->stft.frame_length,
+                (int)c->stft.shift, (int)c->stft.bin_min, (int)c->cfg.bins, cap, slot0};
+    launch_stft(sa, nframes, c->stream);
+    ++c->launches;
+    return check_last_launch("stft_kernel");
+}
+
+// appends up to `n` samples per channel (host, row pitch `ld`) to the
+// sample history; returns the count taken
+int append_samples(sslg_ctx* c, const float* pcm, size_t ld, size_t n, size_t* took) {
+    const size_t take = std::min(n, c->samp_cap - c->samp_fill);
+    if (take)
+        CU(cudaMemcpy2DAsync(c->samp[c->samp_cur] + c->samp_fill, c->samp_cap * sizeof(float), pcm, ld * sizeof(float),
+                             take * sizeof(float), c->cfg.m, cudaMemcpyHostToDevice, c->stream));
+    c->samp_fill += take;
+    *took = take;
+    return 0;
+}
+
+// drops the first `consumed` samples of the history (ping-pong copy of the tail)
+int consume_samples(sslg_ctx* c, size_t consumed) {
+    const size_t tail = c->samp_fill - consumed;
+    if (tail)
+        CU(cudaMemcpy2DAsync(c->samp[c->samp_cur ^ 1], c->samp_cap * sizeof(float), c->samp[c->samp_cur] + consumed,
+                             c->samp_cap * sizeof(float), tail * sizeof(float), c->cfg.m, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    c->samp_cur ^= 1;
+    c->samp_fill = tail;
+    return 0;
+}
+
+uint32_t frames_ready(const sslg_ctx* c) {
+    const size_t L = c->stft.frame_length;
+    if (c->samp_fill < L) return 0;
+    return (uint32_t)std::min<size_t>((c->samp_fill - L) / c->stft.shift + 1, c->cfg.max_batch);
+}
+
+}  // namespace
+
+int sslg_stft(sslg_ctx* c, const float* pcm, uint64_t nsamples, float* frames, uint32_t cap_frames, uint32_t* nframes) {
+    if (!c || !pcm) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
+    CU(cudaSetDevice(c->cfg.device));
+    const size_t L = c->stft.frame_length, S = c->stft.shift;
+    const uint64_t total = nsamples < L ? 0 : (nsamples - L) / S + 1;  // stft_frame_count (stft.cpp:38-42)
+    if (nframes) *nframes = (uint32_t)total;
+    if (!frames) return SSLG_OK;
+    if (total > cap_frames) return set_err(SSLG_VALIDATION, "frame buffer too small for this block");
+    const size_t fsz = (size_t)c->cfg.m * c->cfg.bins;
+    c->launches = 0;
+    // stage the block through the second history buffer, one max_batch chunk at a time
+    float* stage = c->samp[c->samp_cur ^ 1];
+    for (uint64_t f0 = 0; f0 < total; f0 += c->cfg.max_batch) {
+        const int nf = (int)std::min<uint64_t>(total - f0, c->cfg.max_batch);
+        const size_t span = (size_t)(nf - 1) * S + L;
+        CU(cudaMemcpy2DAsync(stage, c->samp_cap * sizeof(float), pcm + f0 * S, nsamples * sizeof(float),
+                             span * sizeof(float), c->cfg.m, cudaMemcpyHostToDevice, c->stream));
+        TRY(launch_stft_frames(c, stage, c->samp_cap, nf, c->frame_scratch, nf, 0));
+        CU(cudaMemcpyAsync(frames + f0 * fsz * 2, c->frame_scratch, nf * fsz * sizeof(float2), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    return SSLG_OK;
+}
+
+int sslg_samples_pending(const sslg_ctx* c, uint64_t nsamples, uint32_t* frames, uint32_t* blocks) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
+    const uint64_t have = c->samp_fill + nsamples, L = c->stft.frame_length;
+    const uint64_t f = have < L ? 0 : (have - L) / c->stft.shift + 1;
+    const long long need = (long long)c->cfg.window_frames - 1 - c->pushed;  // frames still filling the window
+    const long long b = (long long)f - std::max<long long>(0, need);
+    if (frames) *frames = (uint32_t)f;
+    if (blocks) *blocks = (uint32_t)std::max<long long>(0, b);
+    return SSLG_OK;
+}
+
+int sslg_push_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32_t cap_blocks, sslg_block_out* blocks,
+                      uint32_t* est_idx, double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    TRY(require_ready(c));
+    if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
+    if (!pcm && nsamples) return set_err(SSLG_VALIDATION, "null argument");
+    uint32_t need = 0;
+    TRY(sslg_samples_pending(c, nsamples, nullptr, &need));
+    if (need > cap_blocks) return set_err(SSLG_VALIDATION, "result arrays too small for the emitted blocks");
+    const size_t ns = c->cfg.num_sources;
+    uint32_t out = 0, launches = 0;
+    uint64_t off = 0;
+    for (;;) {
+        size_t took = 0;
+        c->launches = 0;
+        TRY(append_samples(c, pcm + off, nsamples, nsamples - off, &took));
+        off += took;
+        const uint32_t nf = frames_ready(c);
+        if (nf == 0) {
+            if (off >= nsamples) break;
+            continue;
+        }
+        TRY(launch_stft_frames(c, c->samp[c->samp_cur], c->samp_cap, (int)nf, c->ring, c->cap, c->pushed));
+        TRY(gate_frames(c, nf));
+        uint32_t e = 0;
+        TRY(process_chunk(c, nf, &e));
+        TRY(consume_samples(c, (size_t)nf * c->stft.shift));
+        launches += c->launches;
+        TRY(sslg_read_results(c, e, blocks ? blocks + out : nullptr, est_idx ? est_idx + out * ns : nullptr,
+                              est_power ? est_power + out * ns : nullptr, est_low ? est_low + out * ns : nullptr,
+                              power ? power + (size_t)out * c->dirs : nullptr, nullptr, nullptr, nullptr, nullptr));
+        out += e;
+    }
+    c->launches = launches;
+    if (emitted) *emitted = out;
+    return SSLG_OK;
+}
+
+int sslg_locate_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32_t cap_blocks, sslg_block_out* blocks,
+                        uint32_t* est_idx, double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(sslg_reset_window(c));
+    c->samp_fill = 0;
+    return sslg_push_samples(c, pcm, nsamples, cap_blocks, blocks, est_idx, est_power, est_low, power, emitted);
 }
 
 }  // extern "C"

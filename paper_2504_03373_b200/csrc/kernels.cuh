@@ -6,6 +6,18 @@
 
 namespace sslg {
 
+struct StftArgs {
+    const float* pcm;        // [m][pitch] samples, channel-major (SampleBlock::channels)
+    const float* window;     // [n] make_window (host-evaluated, stft.cpp:28-36)
+    const double2* twiddle;  // [n-1] per-stage recurrence twiddles, stage len at offset len/2-1
+    float2* out;             // frame ring [cap][m][bins]
+    size_t pitch;            // samples per channel row
+    int m, n, shift, bin_min, bins;
+    int cap;
+    long long slot0;         // ring index of frame 0 of this launch
+};
+void launch_stft(const StftArgs& a, int nframes, cudaStream_t s);
+
 struct CorrArgs {
     const float2* ring;  // [cap][m][bins] spectra, frame g at slot g % cap
     double2* state;      // [bins][m][m] FP64 running sum

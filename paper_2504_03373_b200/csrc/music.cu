@@ -157,6 +157,11 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
             a.est_pw[(size_t)blk * a.ns + k] = pw[best[k]];
             a.est_low[(size_t)blk * a.ns + k] = pw[best[k]] < thr ? 1 : 0;
         }
+        for (int k = nb; k < a.ns; ++k) {  // unused slots: no estimate
+            a.est_idx[(size_t)blk * a.ns + k] = 0xffffffffu;
+            a.est_pw[(size_t)blk * a.ns + k] = 0.0;
+            a.est_low[(size_t)blk * a.ns + k] = 0;
+        }
         a.est_count[blk] = (uint32_t)nb;
     }
 }

@@ -75,6 +75,37 @@ class SolverConfig:
 
 
 @dataclass
+class StftConfig:
+    """ssl::StftConfig (types.hpp:41-52)."""
+
+    frame_length: int = 512
+    shift: int = 160
+    window: str = "hann"  # hann | rectangular (stft.cpp:18-26)
+    bin_min: int = 16
+    bin_max: int = 88
+
+    def bin_count(self) -> int:
+        return self.bin_max - self.bin_min + 1
+
+    def validate(self) -> None:
+        """StftConfig::validate (stft.cpp:9-16)."""
+        if self.frame_length <= 0:
+            raise ValidationError("frame_length must be positive")
+        if self.shift <= 0:
+            raise ValidationError("shift must be positive")
+        if self.shift > self.frame_length:
+            raise ValidationError("shift must not exceed frame_length")
+        if self.bin_min > self.bin_max:
+            raise ValidationError("bin_min must not exceed bin_max")
+        if self.bin_max > self.frame_length // 2:
+            raise ValidationError("bin_max exceeds the half spectrum of frame_length")
+        if self.window not in ("hann", "rectangular", "rect"):
+            raise ValidationError(f"unknown window '{self.window}'")
+        if self.window == "rect":
+            self.window = "rectangular"
+
+
+@dataclass
 class MusicConfig:
     """ssl::MusicConfig (music.hpp:49-62)."""
 
@@ -291,6 +322,62 @@ class Engine:
         return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
                     count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
                     low=low[:n].astype(bool), power=None if power is None else power[:n])
+
+    # ---- STFT front end (SampleBlock in) -----------------------------------
+    def set_stft(self, stft: "StftConfig") -> None:
+        """StftConfig (types.hpp:41-52) for push_samples / locate_samples / stft."""
+        stft.validate()
+        cfg = _capi.StftConfig(stft.frame_length, stft.shift, 0 if stft.window == "hann" else 1, stft.bin_min,
+                               stft.bin_max)
+        _capi.check(self.L.sslg_set_stft(self.h, C.byref(cfg)))
+        self.stft_cfg = stft
+
+    def stft(self, pcm: np.ndarray) -> np.ndarray:
+        """stft_stream of one SampleBlock pcm [m][n] float32 -> frames
+        [F][m][bins] complex64, bit-identical to the reference (stft.cpp:44-68)."""
+        pcm = np.ascontiguousarray(pcm, np.float32)
+        n = C.c_uint32()
+        _capi.check(self.L.sslg_stft(self.h, f32p(pcm), pcm.shape[1], None, 0, C.byref(n)))
+        out = np.zeros((n.value, self.m, self.bins), np.complex64)
+        if n.value:
+            _capi.check(self.L.sslg_stft(self.h, f32p(pcm), pcm.shape[1], f32p(out), n.value, C.byref(n)))
+        return out
+
+    def _samples_call(self, fn, pcm: np.ndarray, want_power: bool):
+        pcm = np.ascontiguousarray(pcm, np.float32)
+        if pcm.ndim != 2 or pcm.shape[0] != self.m:
+            raise ValidationError("sample block channel count does not match the engine")
+        nb = C.c_uint32()
+        if fn is self.L.sslg_locate_samples:
+            fr = C.c_uint32()
+            _capi.check(self.L.sslg_stft(self.h, f32p(pcm), pcm.shape[1], None, 0, C.byref(fr)))
+            cap = max(fr.value - self.T + 1, 0)
+        else:
+            _capi.check(self.L.sslg_samples_pending(self.h, pcm.shape[1], None, C.byref(nb)))
+            cap = nb.value
+        ns = self.music.num_sources
+        blocks = (_capi.BlockOut * max(cap, 1))()
+        idx = np.zeros((cap, ns), np.uint32)
+        pw = np.zeros((cap, ns))
+        low = np.zeros((cap, ns), np.uint8)
+        power = np.zeros((cap, self.dirs)) if want_power else None
+        em = C.c_uint32()
+        _capi.check(fn(self.h, f32p(pcm), pcm.shape[1], cap, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
+                       C.byref(em)))
+        n = em.value
+        return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
+                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
+                    low=low[:n].astype(bool), power=None if power is None else power[:n])
+
+    def push_samples(self, pcm: np.ndarray, want_power: bool = False):
+        """Streaming: appends pcm [m][n] float32 to the sample history and runs
+        every completed frame through the hot path (frames continue across
+        calls)."""
+        return self._samples_call(self.L.sslg_push_samples, pcm, want_power)
+
+    def locate_samples(self, pcm: np.ndarray, want_power: bool = False):
+        """run_locate over one SampleBlock (pipeline.cpp:210-247): fresh window."""
+        return self._samples_call(self.L.sslg_locate_samples, pcm, want_power)
 
     def push_device(self, x_dev_ptr: int, nframes: int) -> int:
         em = C.c_uint32()
@@ -638,6 +725,47 @@ def run_locate(frames: np.ndarray, window_frames: int, noise: NoiseModel, steeri
                                            bool(out["low"][b, i])))
             if sink:
                 sink(FrameEstimates(first_frame_index + int(out["frame_index"][b]), ests))
+        return int(out["n"])
+    finally:
+        eng.close()
+
+
+def run_locate_samples(audio: np.ndarray, stft: StftConfig, window_frames: int, noise: NoiseModel,
+                       steering: SteeringField, solver: Optional[SolverConfig] = None,
+                       music: Optional[MusicConfig] = None, sink: Optional[Callable[[FrameEstimates], None]] = None,
+                       threads: int = 0, topology: Optional[DirectionTopology] = None, max_batch: int = 16) -> int:
+    """run_locate (pipeline.hpp:71-75, pipeline.cpp:210-247) on a SampleBlock
+    audio [m][samples] float32: device STFT -> correlation window -> GSVD ->
+    MUSIC -> peaks; the sink receives one FrameEstimates per emitted frame.
+    `threads` is accepted for signature parity (results never depend on it)."""
+    music = music or MusicConfig()
+    solver = solver or SolverConfig()
+    steering.validate()
+    stft.validate()
+    if window_frames == 0:
+        raise ValidationError("window_frames must be at least 1")
+    if noise.k.m != steering.m:
+        raise ValidationError("noise model channel count does not match steering field")
+    if noise.k.bin_count() != stft.bin_count():
+        raise ValidationError("noise model bin count does not match the analysis band")
+    audio = np.ascontiguousarray(audio, np.float32)
+    eng = Engine(steering.m, steering.bin_count(), window_frames=window_frames, music=music, solver=solver,
+                 max_batch=max_batch)
+    try:
+        eng.set_noise_model(noise.k.bins)
+        topo = topology or DirectionTopology.build(steering.directions)
+        eng.set_steering(steering.vectors, steering.directions, topo)
+        eng.set_stft(stft)
+        out = eng.locate_samples(audio)
+        dirs = _dirs_array(steering.directions)
+        for b in range(out["n"]):
+            ests = []
+            for i in range(int(out["count"][b])):
+                j = int(out["idx"][b, i])
+                ests.append(SourceEstimate(j, Direction(*dirs[j]), float(out["power_est"][b, i]),
+                                           bool(out["low"][b, i])))
+            if sink:
+                sink(FrameEstimates(int(out["frame_index"][b]), ests))
         return int(out["n"])
     finally:
         eng.close()

@@ -91,7 +91,33 @@ def kat_fixture():
     print("kat", len(out), "arrays")
 
 
+def stft_fixture():
+    """Audio through the reference's stft_stream (stft.cpp:38-68, fft.hpp:15-68):
+    PCM from synthesize_scene, frames from the reference itself."""
+    R = oracle.ref()
+    out = {}
+    cases = [
+        ("hann_band", Scene(mics=8, radius=0.05, duration_s=0.25, seed=21, diffuse_db=-20, bin_min=16, bin_max=88,
+                            sources=[Source(40), Source(150, kind="tone", freq=1000.0)])),
+        ("rect_full", Scene(mics=3, radius=0.05, duration_s=0.12, seed=4, window="rectangular", bin_min=0,
+                            bin_max=256, sources=[Source(10), Source(200, kind="tone", freq=2500.0)])),
+        ("hann_256", Scene(mics=5, radius=0.05, duration_s=0.1, seed=8, frame_length=256, shift=100, bin_min=3,
+                           bin_max=128, diffuse_db=-10, sources=[Source(300)])),
+    ]
+    for name, sc in cases:
+        w = R.workload(sc, with_audio=True)
+        out[f"{name}_audio"] = w.audio
+        out[f"{name}_frames"] = w.x
+        out[f"{name}_cfg"] = np.array([sc.frame_length, sc.shift, 0 if sc.window == "hann" else 1, sc.bin_min,
+                                       sc.bin_max], np.int64)
+        print("stft", name, w.audio.shape, "->", w.x.shape)
+    np.savez_compressed(os.path.join(HERE, "stft.npz"), **out)
+
+
 def main():
+    if "--stft" in sys.argv:
+        stft_fixture()
+        return
     # C1 shape, reduced band: 8-ch circular, 2 white sources + diffuse, captured K
     scene_fixture("c1_band", Scene(mics=8, radius=0.05, duration_s=0.5, seed=7, diffuse_db=-20, bin_min=16,
                                    bin_max=48, sources=[Source(40), Source(150)], noise="captured"),
@@ -107,6 +133,7 @@ def main():
                                                                     Source(250)], noise="identity"),
                   t=6, ns=2, frames=10)
     kat_fixture()
+    stft_fixture()
 
 
 if __name__ == "__main__":
