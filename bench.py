@@ -40,6 +40,18 @@ UNIT = "blocks/s"
 REALTIME_BLOCKS_PER_S = 100.0  # fs / shift = 16000 / 160 per array
 
 
+WORKLOADS = {"c1": "C1 (BASELINE configs[0])", "c2": "C2 (BASELINE configs[1])", "c3": "C3 (BASELINE configs[2])",
+             "c4": "C4 (BASELINE configs[3], 72 az x 19 el grid)"}
+
+
+def frames_from_pcm(w):
+    """The scene's STFT frames for the CPU arms (oracle restatement of
+    stft_stream, bit-identical to the reference and to the device STFT)."""
+    import oracle
+
+    return oracle.port().stft(w.pcm, w.frame_length, w.shift, 0, w.bin_min, w.bin_max)
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -211,8 +223,10 @@ def main():
 
     from paper_2504_03373_b200 import synth
 
-    frames_needed = 50 + (args.warmup + args.steps + 1) * args.batch
-    w = synth.make(args.config, frames=max(frames_needed, 120), seed=11 + rank)
+    # the scene as PCM (SampleBlock): the product path runs the device STFT
+    # front end; the reference arm and the cpu_baseline see the same frames
+    frames_needed = 50 + (args.warmup + args.steps + 1) * args.batch + 8
+    w = synth.make_pcm(args.config, duration_s=((frames_needed - 1) * 160 + 512) / 16000.0, seed=11 + rank)
 
     if args.impl == "reference":
         try:
@@ -224,6 +238,7 @@ def main():
             if rank == 0:
                 print(json.dumps({"impl": "reference", "unavailable": str(e).splitlines()[0]}), flush=True)
             return
+        w.x = frames_from_pcm(w)
         run_reference_arm(args, w, rank, world)
         return
 
@@ -247,6 +262,8 @@ def main():
                      max_batch=args.batch, device=device, stream=stream.cuda_stream)
     eng.set_noise_model(w.k)
     eng.set_steering(w.h, w.dirs)
+    eng.set_stft(ssl.StftConfig(w.frame_length, w.shift, "hann", w.bin_min, w.bin_max))
+    w.x = eng.stft(w.pcm)  # the device STFT of the scene (bit-identical to the reference's)
 
     # inputs resident in HBM before the timed region
     x_all = torch.from_numpy(w.x.view(np.float32)).to(f"cuda:{device}")  # [F][m][bins*2]
@@ -322,20 +339,28 @@ def main():
         lat.append(1e3 * float(s[1] + s[2]))
     gsvd_latency_us = float(np.median(lat))
 
-    # e2e: the public C-ABI entry with host buffers (pinned), H2D + D2H inside
-    pinned = torch.from_numpy(w.x.view(np.float32)).pin_memory()
+    # e2e: run_locate's public entry on SampleBlocks (sslg_push_samples): per
+    # step, batch * shift new samples per channel from pinned host memory go
+    # H2D, the device STFT turns them into frames inside the window, the hot
+    # path runs, and the estimates come back D2H -- all inside the timed region
+    eng.reset_window()
+    step_samples = args.batch * w.shift
+    lead = (w.t - 1) * w.shift + w.frame_length - w.shift  # fills the window to T-1 frames
+    nchunks = args.warmup + args.steps
+    need = lead + nchunks * step_samples
+    src = w.pcm if w.pcm.shape[1] >= need else np.tile(w.pcm, (1, need // w.pcm.shape[1] + 1))
+    chunks = [torch.from_numpy(np.ascontiguousarray(src[:, lead + i * step_samples:lead + (i + 1) * step_samples]))
+              .pin_memory() for i in range(nchunks)]
+    eng.push_samples(np.ascontiguousarray(src[:, :lead]))
     e2e_ms = []
     ns = w.ns
-    hpos = w.t
-    for i in range(args.warmup + args.steps):
-        if hpos + args.batch > pinned.shape[0]:
-            hpos = w.t
-        xh = pinned[hpos:hpos + args.batch].numpy().view(np.complex64)
-        hpos += args.batch
+    for i in range(nchunks):
+        xh = chunks[i].numpy()
         sync_all()
         t0 = time.perf_counter()
-        out = eng.push(xh)
+        out = eng.push_samples(xh)
         dt = time.perf_counter() - t0
+        assert out["n"] == args.batch
         if i >= args.warmup:
             e2e_ms.append(dt * 1e3)
     e2e_total = float(sum(e2e_ms))
@@ -344,7 +369,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
     e2e_value = world * args.steps * args.batch / (e2e_total * 1e-3)
-    h2d = args.batch * fsz * 8
+    h2d = w.m * step_samples * 4
     d2h = args.batch * (ns * (4 + 8 + 1) + 8)
 
     if rank == 0:
@@ -390,9 +415,10 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C3 (BASELINE configs[2]): {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, "
-                                   f"{w.bins} bins, {w.h.shape[0]} azimuths, 2 targets + 4 rotor sources + diffuse, "
-                                   f"captured K, T={w.t}, Ns={w.ns}",
+            "config": {"workload": f"{WORKLOADS[args.config]}: {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, "
+                                   f"{w.bins} bins, {w.h.shape[0]} directions, {w.ns} targets (0 dB) + 4 rotor "
+                                   f"sources (-10 dB) + diffuse (-20 dB), K captured from a noise-only recording, "
+                                   f"T={w.t}, Ns={w.ns}; PCM input, device STFT",
                        "blocks_per_step_per_gpu": args.batch, "arrays": world,
                        "l2": "flushed (256 MiB write) between timed steps" if not args.no_flush else "not flushed",
                        "parallelism": f"array-sharded x{world} (no data-path collective)"},
@@ -404,7 +430,8 @@ def main():
             "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "sslg_push_frames (host buffers)"},
+                    "api": "sslg_push_samples (run_locate on pinned host PCM: H2D, device STFT, hot path, "
+                           "estimates D2H)"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -434,7 +461,15 @@ def cpu_baseline(w, nblocks):
         return None
     cores = os.cpu_count() or 1
     spb, st = reference_time_blocks(w, nblocks, cores)
+    # the paper's methodology: gsvd() with one thread ("naive" path), 2 blocks
+    R = oracle.ref()
+    r = R.correlation(w.x[:w.t + 1], w.t)
+    t0 = time.perf_counter()
+    for rb in r[:2]:
+        R.gsvd(w.k, rb, path=0, threads=1)
+    gsvd_1t_us = 1e6 * (time.perf_counter() - t0) / 2
     return {"value": 1.0 / spb, "unit": UNIT, "cores": cores, "kind": "reference",
+            "gsvd_1thread_us_per_block": gsvd_1t_us,
             "sample": f"{nblocks} consecutive blocks of the same C3 stream through the reference run_locate loop "
                       f"(oracle/_ref = unmodified sslkit, ssl::gsvd batched float path, {cores} threads)",
             "stage_s": {"correlation": st[0], "factorization": st[1], "spectrum": st[2], "peaks": st[3]},

@@ -129,8 +129,10 @@ CONFIGS = {
     # BASELINE.json configs[0..4]
     "c1": dict(m=8, radius=0.05, targets_deg=(40.0, 150.0), target_db=0.0, rotors_deg=(), diffuse_db=-20.0, ns=2),
     "c2": dict(m=16, radius=0.05, targets_deg=(75.0, 200.0), target_db=0.0, rotors_deg=(300.0,), ns=2),
-    "c3": dict(m=60, radius=0.3, ns=2),
-    "c4": dict(m=60, radius=0.3, ns=3, targets_deg=(40.0, 150.0, 260.0)),
+    # targets at 0 dB each under four rotors at -10 dB each (-4 dB total) and a
+    # -20 dB diffuse floor: ~ +4 dB per target against the whole noise field
+    "c3": dict(m=60, radius=0.3, ns=2, target_db=0.0, rotor_db=-10.0),
+    "c4": dict(m=60, radius=0.3, ns=3, targets_deg=(40.0, 150.0, 260.0), target_db=0.0, rotor_db=-10.0),
 }
 
 
@@ -139,3 +141,94 @@ def make(config: str, frames: int = 400, seed: int = 11) -> Workload:
     if config == "c4":
         kw["dirs"] = azel_grid(5.0)
     return drone_scene(name=config, frames=frames, seed=seed, **kw)
+
+
+# ---------------------------------------------------------------------------
+# time-domain scenes (SampleBlock input for the STFT front end)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class PcmWorkload:
+    name: str
+    pcm: np.ndarray  # [m][samples] float32 (SampleBlock::channels)
+    k: np.ndarray  # [bins][m][m] complex64
+    h: np.ndarray  # [dirs][bins][m] complex64
+    dirs: np.ndarray  # [dirs][2]
+    t: int
+    ns: int
+    bin_min: int
+    bin_max: int
+    frame_length: int = 512
+    shift: int = 160
+    targets: List[int] = field(default_factory=list)
+
+    @property
+    def m(self):
+        return self.pcm.shape[0]
+
+    @property
+    def bins(self):
+        return self.bin_max - self.bin_min + 1
+
+
+def _pcm_field(rng, mics, src_dirs, levels_db, n, sample_rate, diffuse_db):
+    """Far-field white sources delayed per microphone by tau = -(u . p) / c
+    (the make_steering convention, synth.cpp:123-149: mic spectrum = S(f)
+    exp(-j 2 pi f tau)), applied as an exact frequency-domain delay over the
+    whole signal, plus an independent diffuse floor per microphone."""
+    m = mics.shape[0]
+    f = np.fft.rfftfreq(n, 1.0 / sample_rate)
+    x = np.zeros((m, n))
+    if len(src_dirs):
+        u = unit(np.asarray(src_dirs, np.float64))  # [S][3]
+        tau = -(u @ mics.T) / SPEED_OF_SOUND  # [S][m]
+        for s, lvl in enumerate(levels_db):
+            spec = np.fft.rfft(rng.standard_normal(n) * 10 ** (lvl / 20.0))
+            x += np.fft.irfft(spec[None, :] * np.exp(-2j * np.pi * f[None, :] * tau[s][:, None]), n)
+    if diffuse_db is not None:
+        x += rng.standard_normal((m, n)) * 10 ** (diffuse_db / 20.0)
+    return x
+
+
+def _stft_np(x, frame_length, shift, bin_min, bin_max):
+    """Periodic-Hann STFT (numpy; used only to capture K from noise-only PCM)."""
+    w = 0.5 - 0.5 * np.cos(2 * np.pi * np.arange(frame_length) / frame_length)
+    nf = (x.shape[1] - frame_length) // shift + 1
+    idx = np.arange(frame_length)[None, :] + shift * np.arange(nf)[:, None]
+    fr = np.fft.rfft(x[:, idx] * w[None, None, :], axis=2)[:, :, bin_min:bin_max + 1]  # [m][F][bins]
+    return fr.transpose(1, 2, 0)  # [F][bins][m]
+
+
+def drone_scene_pcm(name: str = "c3", m: int = 60, radius: float = 0.3, bin_min: int = 0, bin_max: int = 256,
+                    dirs: np.ndarray = None, duration_s: float = 2.0, t: int = 50, ns: int = 2,
+                    targets_deg: Sequence[float] = (40.0, 150.0), target_db: float = -3.0,
+                    rotors_deg: Sequence[float] = (45.0, 135.0, 225.0, 315.0), rotor_db: float = 0.0,
+                    diffuse_db: float = -20.0, noise_s: float = 2.5, seed: int = 11, frame_length: int = 512,
+                    shift: int = 160, sample_rate: int = 16000) -> PcmWorkload:
+    """The C3 drone scene as PCM: targets under four rotor sources and a
+    diffuse floor; K captured from a separate noise-only recording
+    (capture_noise_model, synth.cpp:329-373)."""
+    rng = np.random.default_rng(seed)
+    mics = circular(m, radius)
+    dirs = azimuth_grid(5.0) if dirs is None else dirs
+    src = [(a, 0.0) for a in targets_deg] + [(a, 0.0) for a in rotors_deg]
+    lv = [target_db] * len(targets_deg) + [rotor_db] * len(rotors_deg)
+    n = int(duration_s * sample_rate)
+    pcm = _pcm_field(rng, mics, src, lv, n, sample_rate, diffuse_db).astype(np.float32)
+    noise = _pcm_field(rng, mics, [(a, 0.0) for a in rotors_deg], [rotor_db] * len(rotors_deg),
+                       int(noise_s * sample_rate), sample_rate, diffuse_db)
+    fr = _stft_np(noise, frame_length, shift, bin_min, bin_max)
+    k = (np.einsum("fbi,fbj->bij", fr, fr.conj()) / fr.shape[0]).astype(np.complex64)
+    h = steering(mics, dirs, bin_min, bin_max, frame_length, sample_rate)
+    tgt = [int(np.argmin(np.abs(dirs[:, 0] - a) + np.abs(dirs[:, 1]))) for a in targets_deg]
+    return PcmWorkload(name, pcm, k, h, np.ascontiguousarray(dirs, np.float64), t, ns, bin_min, bin_max,
+                       frame_length, shift, tgt)
+
+
+def make_pcm(config: str, duration_s: float = 2.0, seed: int = 11) -> PcmWorkload:
+    kw = dict(CONFIGS[config])
+    kw.pop("geometry", None)
+    if config == "c4":
+        kw["dirs"] = azel_grid(5.0)
+    return drone_scene_pcm(name=config, duration_s=duration_s, seed=seed, **kw)

@@ -62,6 +62,8 @@ def test_c3_blocks_against_oracle(port):
     w, out, res, want = _run("c3", 53, port)
     assert out["n"] == 4
     _check(out, res, want)
+    # the scene's two targets are the two reported sources
+    assert set(out["idx"][0][:2].tolist()) == set(w.targets)
 
 
 def test_c4_azel_grid_against_oracle(port):
