@@ -91,17 +91,26 @@ __device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) 
             if (e < nc * nd && (t & 3) == 0) G[e] = d;
         }
         __syncthreads();
-        // w_D[b][i] -= sum_a G[a][b] e_C[a][i]
+        // w_D[b][i] -= sum_a G[a][b] e_C[a][i]  (four independent partial sums)
         for (int o = t; o < nd * m; o += nt) {
             const int b = o / m, i = o % m;
-            double2 acc = make_double2(0, 0);
-            for (int a = 0; a < nc; ++a) {
+            double2 acc[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+            int a = 0;
+            for (; a + 4 <= nc; a += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double2 g = G[(a + u) * nd + b], ev = W[cs.certcols[a + u] * m + i];
+                    acc[u].x = fma(g.x, ev.x, fma(-g.y, ev.y, acc[u].x));
+                    acc[u].y = fma(g.x, ev.y, fma(g.y, ev.x, acc[u].y));
+                }
+            }
+            for (; a < nc; ++a) {
                 const double2 g = G[a * nd + b], ev = W[cs.certcols[a] * m + i];
-                acc.x = fma(g.x, ev.x, fma(-g.y, ev.y, acc.x));
-                acc.y = fma(g.x, ev.y, fma(g.y, ev.x, acc.y));
+                acc[0].x = fma(g.x, ev.x, fma(-g.y, ev.y, acc[0].x));
+                acc[0].y = fma(g.x, ev.y, fma(g.y, ev.x, acc[0].y));
             }
             double2* w = W + cs.dropped[b] * m + i;
-            *w = csub(*w, acc);
+            *w = csub(*w, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
         }
         __syncthreads();
     }
@@ -145,7 +154,7 @@ __device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) 
                     }
                     break;
                 }
-                const double ljj = sqrt(gjj), inv = 1.0 / ljj;
+                const double inv = fast_rsqrt(gjj);
                 for (int i = j + 1 + t; i < nd; i += kWarp) {
                     double2& gij = G[i * (i + 1) / 2 + j];
                     gij = cscale(inv, gij);
@@ -195,10 +204,85 @@ __device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) 
     }
 }
 
+// Fast path of the picker: when the first d candidates (rows 0..d-1 of
+// conj(N)) are all accepted in the first pass — the usual case, a unit
+// vector projects onto a d-dimensional span with norm ~sqrt(d/m) >> 0.05 —
+// the reference's sequential two-pass Gram-Schmidt over them is the QR
+// factorization Y = Z R of the d x d candidate matrix, and candidate j's
+// residual norm is R_jj.  One warp forms G = Y^H Y, runs the Cholesky
+// G = R^H R checking R_jj > 0.05 n0_j at every step (the acceptance test of
+// pick_orthonormal, gsvd.cpp:404-436), and forms Z = Y R^-1.  Returns false
+// (nothing written) when a candidate would be rejected; the caller then runs
+// the sequential picker.  No block barrier inside: warp 0 only.
+__device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_norm0, CanonScratch& cs) {
+    __shared__ int s_ok;
+    const int t = threadIdx.x;
+    if (t < kWarp) {
+        const int lane = t;
+        // G[a][b] = y_a^H y_b,  y_j[k] = conj(W[cols[k]][j])
+        for (int e = lane; e < d * d; e += kWarp) {
+            const int a = e / d, b = e % d;
+            if (b < a) continue;
+            double gx = 0, gy = 0;
+            for (int k = 0; k < d; ++k) {
+                const double2 wa = W[cs.cols[k] * m + a], wb = W[cs.cols[k] * m + b];
+                // conj(y_a) y_b = wa * conj(wb)
+                gx = fma(wa.x, wb.x, fma(wa.y, wb.y, gx));
+                gy = fma(wa.y, wb.x, fma(-wa.x, wb.y, gy));
+            }
+            G[a * d + b] = make_double2(gx, gy);
+        }
+        __syncwarp();
+        if (lane < d) cs.norm0[lane] = unit_norm0 ? 1.0 : sqrt(G[lane * d + lane].x);
+        __syncwarp();
+        bool ok = true;
+        for (int j = 0; j < d && ok; ++j) {
+            const double gjj = G[j * d + j].x;
+            const double n0 = cs.norm0[j];
+            const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
+            if (!(n0 > 1e-140) || !(rjj > 0.05 * n0) || !(rjj > 0)) {
+                ok = false;
+                break;
+            }
+            const double inv = 1.0 / rjj;
+            for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
+            __syncwarp();
+            // trailing upper triangle: G[a][b] -= conj(R[j][a]) R[j][b], j < a <= b
+            const int n = d - j - 1;
+            for (int e = lane; e < n * n; e += kWarp) {
+                const int a = j + 1 + e / n, b = j + 1 + e % n;
+                if (b < a) continue;
+                const double2 ra = G[j * d + a], rb = G[j * d + b];
+                double2& g = G[a * d + b];
+                g.x -= fma(ra.x, rb.x, ra.y * rb.y);
+                g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+            }
+            if (lane == 0) {
+                G[j * d + j] = make_double2(rjj, 0.0);
+                cs.nrm[j] = inv;
+            }
+            __syncwarp();
+        }
+        if (ok && lane < d) {  // Z = Y R^-1 column by column, lane = coordinate
+            const int k = lane;
+            for (int tt = 0; tt < d; ++tt) {
+                const double2 w = W[cs.cols[k] * m + tt];
+                double2 acc = make_double2(w.x, -w.y);  // y_tt[k]
+                for (int s2 = 0; s2 < tt; ++s2) acc = csub(acc, cmul(cs.z[k][s2], G[s2 * d + tt]));
+                cs.z[k][tt] = cscale(cs.nrm[tt], acc);
+            }
+        }
+        if (lane == 0) s_ok = ok ? 1 : 0;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
 // Reference picker (pick_orthonormal, gsvd.cpp:404-436) on the coordinates of
 // one group: candidate j is row j of conj(N), N = W[cols[0..d)].  Threads
 // j < m own candidate j; the accepted coordinate vectors land in cs.z.
 __device__ void pick_in_span(const double2* W, double2* Y, int m, int d, bool unit_norm0, CanonScratch& cs) {
+    if (d <= kZMax && pick_fast(W, Y, m, d, unit_norm0, cs)) return;
     const int t = threadIdx.x;
     double2* yr = Y + t * kYld;
     bool used = false;
@@ -616,7 +700,7 @@ __device__ __forceinline__ void japply(double2 (&P)[RPL], double2 (&Q)[RPL], con
 // column.  Returns whether a rotation was applied.
 template <int R, int L>
 __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], double& cp, double& cq, double drop,
-                                            int s, int m) {
+                                            int s, int m, double& maxrel) {
     double d0x = 0, d0y = 0, d1x = 0, d1y = 0;
 #pragma unroll
     for (int u = 0; u < R; ++u) {
@@ -633,6 +717,7 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
     const double2 dot = group_sum2<L>(make_double2(d0x + d1x, d0y + d1y));
     const double mag2 = fma(dot.x, dot.x, dot.y * dot.y);
     if (cp <= drop || cq <= drop || mag2 <= 1e-28 * cp * cq) return false;
+    if (mag2 > 1e-16 * cp * cq) maxrel = 1.0;  // a coupling above 1e-8 relative was rotated
     japply<R>(P, Q, jrot(dot.x, dot.y, cp, cq), cp, cq);
     return true;
 }
@@ -734,8 +819,13 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     const int npairs = n_even / 2;
 
     __shared__ int s_rots;
-    if (tid == 0) s_rots = 0;
+    __shared__ unsigned long long s_maxrel;  // 1: a pair coupled above 1e-8 relative was rotated this sweep
+    if (tid == 0) {
+        s_rots = 0;
+        s_maxrel = 0ull;
+    }
     int prev_rots = 1 << 30;
+    double prev_maxrel = 1.0;
     const int total_pairs = m * (m - 1) / 2;
     int sweep = 0;
     bool converged = false;
@@ -771,14 +861,20 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         }
         __syncthreads();
         const double drop = s_drop;
-        // A sweep after one that rotated few pairs is usually rotation-free:
-        // certify that with one Gram product instead of running it.
-        if (sweep > 0 && 16 * prev_rots < total_pairs && gram_converged(W, m, cn, drop)) {
+        // A sweep after one that rotated few pairs, or only pairs coupled by
+        // <= 1e-8 relative (whose rotations leave couplings ~1e-16, squared
+        // far below the 1e-28 test), is usually rotation-free: certify that
+        // with one Gram product instead of running it.
+        if (sweep > 0 && (16 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged(W, m, cn, drop)) {
             converged = true;
             break;
         }
-        if (tid == 0) s_rots = 0;
+        if (tid == 0) {
+            s_rots = 0;
+            s_maxrel = 0ull;
+        }
         int myrots = 0;
+        double mymax = 0.0;
         bool rot = false;
         // round-robin (circle) ordering: the m/2 disjoint pairs of a round
         // rotate concurrently, one kLPP-lane group per pair
@@ -795,7 +891,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
                         Q[u] = row < m ? W[q * m + row] : make_double2(0, 0);
                     }
                     double cp = cn[p], cq = cn[q];
-                    if (rotate_pair<kRows, kLPP>(P, Q, cp, cq, drop, s, m)) {
+                    if (rotate_pair<kRows, kLPP>(P, Q, cp, cq, drop, s, m, mymax)) {
 #pragma unroll
                         for (int u = 0; u < kRows; ++u) {
                             const int row = s + u * kLPP;
@@ -816,12 +912,16 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
             __syncthreads();
         }
         ++sweep;
-        if (myrots) atomicAdd(&s_rots, myrots);
+        if (myrots) {
+            atomicAdd(&s_rots, myrots);
+            if (mymax > 0) atomicMax(&s_maxrel, 1ull);
+        }
         if (!__syncthreads_or(rot)) {
             converged = true;
             break;
         }
         prev_rots = s_rots;
+        prev_maxrel = s_maxrel ? 1.0 : 0.0;
     }
 
     mark(2);
