@@ -81,6 +81,105 @@ __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
     }
 }
 
+
+// Register-tiled variant for large grids (C4: 1368 directions): each thread
+// owns a 4-direction x 4-vector tile of h^H e products, so one mic step loads
+// 4 steering + 4 noise values for 16 complex MACs (64 FP64 FMAs).  The noise
+// vectors are staged transposed ([mic][vector], padded to 64) and the
+// steering chunk as [mic][direction], so a warp's loads are contiguous and
+// conflict-free.  The 16 threads holding the same directions and different
+// vector slices are adjacent lanes; their partial denominators meet in a
+// 4-level shuffle tree, identical for every direction (exact ties survive).
+constexpr int kTileD = 4, kTileN = 4, kSlices = 16, kDirTiles = 16;
+constexpr int kChunk2 = kTileD * kDirTiles;  // 64 directions per CTA
+constexpr int kNPad = kTileN * kSlices;      // 64 vector slots
+constexpr int kEStride = kNPad + 1;          // double2 row stride of the staged noise vectors (bank spread)
+constexpr int kHStride = kChunk2 + 2;        // float2 row stride of the staged steering (16-B aligned rows)
+
+__global__ void __launch_bounds__(256, 2) spectrum_tiled_kernel(SpecArgs a, int nblk, int nchunk) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = a.m;
+    const int nn = m - a.ns;
+    double2* Et = reinterpret_cast<double2*>(smem_raw);                 // [m][kEStride]
+    float2* Hs = reinterpret_cast<float2*>(Et + (size_t)m * kEStride);  // [m][kHStride]
+    // linear CTA index = (bin * nblk + block) * nchunk + chunk: the chunks of
+    // one (block, bin) run back to back (its noise vectors stay in L2) and
+    // the blocks of one bin follow each other (its steering stays in L2)
+    const int chunk = blockIdx.x % nchunk;
+    const int bb = blockIdx.x / nchunk;
+    const int bin = bb / nblk, blk = bb % nblk;
+    const int blkbin = blk * a.bins + bin;
+    const int d0 = chunk * kChunk2;
+    const int nd = min(kChunk2, a.dirs - d0);
+    const int t = threadIdx.x;
+
+    // staging: coalesced global reads, transposed shared writes (padded strides)
+    const double2* eb = a.e + ((size_t)blkbin * m + a.ns) * m;  // [nn][m]
+    for (int x = t; x < kNPad * m; x += blockDim.x) {
+        const int v = x / m, mic = x % m;
+        Et[mic * kEStride + v] = v < nn ? eb[(size_t)v * m + mic] : make_double2(0, 0);
+    }
+    const float2* hb = a.h + ((size_t)bin * a.dirs + d0) * m;
+    for (int x = t; x < kChunk2 * m; x += blockDim.x) {
+        const int d = x / m, mic = x % m;
+        Hs[mic * kHStride + d] = d < nd ? hb[(size_t)d * m + mic] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+
+    const int slice = t % kSlices, dtile = t / kSlices;
+    double2 acc[kTileD][kTileN];
+#pragma unroll
+    for (int i = 0; i < kTileD; ++i)
+#pragma unroll
+        for (int j = 0; j < kTileN; ++j) acc[i][j] = make_double2(0, 0);
+    const float2* hrow = Hs + dtile * kTileD;
+    const double2* erow = Et + slice;  // vectors slice, slice + 16, ...: lanes read consecutive 16 B
+#pragma unroll 2
+    for (int mic = 0; mic < m; ++mic) {
+        const float4 h01 = *reinterpret_cast<const float4*>(hrow + mic * kHStride);
+        const float4 h23 = *reinterpret_cast<const float4*>(hrow + mic * kHStride + 2);
+        const double2 h[kTileD] = {make_double2(h01.x, h01.y), make_double2(h01.z, h01.w),
+                                   make_double2(h23.x, h23.y), make_double2(h23.z, h23.w)};
+        double2 e[kTileN];
+#pragma unroll
+        for (int j = 0; j < kTileN; ++j) e[j] = erow[mic * kEStride + j * kSlices];
+#pragma unroll
+        for (int i = 0; i < kTileD; ++i)
+#pragma unroll
+            for (int j = 0; j < kTileN; ++j) {  // conj(h) e
+                acc[i][j].x = fma(h[i].x, e[j].x, fma(h[i].y, e[j].y, acc[i][j].x));
+                acc[i][j].y = fma(h[i].x, e[j].y, fma(-h[i].y, e[j].x, acc[i][j].y));
+            }
+    }
+    double den[kTileD];
+#pragma unroll
+    for (int i = 0; i < kTileD; ++i) {
+        double sum = 0;
+#pragma unroll
+        for (int j = 0; j < kTileN; ++j) {
+            const double mag = hypot(acc[i][j].x, acc[i][j].y);
+            sum += a.squared ? mag * mag : mag;
+        }
+        den[i] = sum;
+    }
+#pragma unroll
+    for (int o = kSlices / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < kTileD; ++i) den[i] += __shfl_xor_sync(0xffffffffu, den[i], o);
+    if (slice < kTileD) {
+        const int d = dtile * kTileD + slice;
+        double dd = den[0];
+#pragma unroll
+        for (int i = 1; i < kTileD; ++i)
+            if (slice == i) dd = den[i];
+        if (d < nd) {
+            if (dd < a.floor_) dd = a.floor_;
+            const double num = a.num[(size_t)bin * a.dirs + d0 + d];
+            a.p[(size_t)blkbin * a.dirs + d0 + d] = num / dd;
+        }
+    }
+}
+
 // |h|^2 per (bin, dir) in the reference's order: sequential over mics,
 // (re^2 + im^2) rounded once (both squares exact in double).
 __global__ void steering_prep_kernel(const float2* __restrict__ h_in,  // [dirs][bins][m]
@@ -178,6 +277,13 @@ void spectrum_shape(int m, int ns, int dirs, int& dchunk, int& nsplit, size_t& s
 }
 
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
+    if (a.dirs >= 256 && a.m - a.ns <= kNPad) {  // large grids: register-tiled kernel
+        const size_t smem2 = (size_t)a.m * kEStride * sizeof(double2) + (size_t)a.m * kHStride * sizeof(float2);
+        cudaFuncSetAttribute(spectrum_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        const int nchunk = (a.dirs + kChunk2 - 1) / kChunk2;
+        spectrum_tiled_kernel<<<nblk * a.bins * nchunk, 256, smem2, s>>>(a, nblk, nchunk);
+        return;
+    }
     size_t smem;
     spectrum_shape(a.m, a.ns, a.dirs, a.dchunk, a.nsplit, smem);
     cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
