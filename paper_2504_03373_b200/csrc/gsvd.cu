@@ -601,8 +601,10 @@ __device__ void back_multiply(double2* W, const double2* __restrict__ ag, int m,
     int parts = blockDim.x / m;
     if (parts > m) parts = m;
     const bool active = t < m * parts;
-    const int i = active ? t / parts : 0;
-    const int part = active ? t % parts : 0;
+    // part-major: a warp covers consecutive rows i of one column set, so its
+    // W reads are broadcasts and its A loads coalesce
+    const int i = active ? t % m : 0;
+    const int part = active ? t / m : 0;
     const int per = (m + parts - 1) / parts;  // columns per thread
     for (int u0 = 0; u0 < per; u0 += 8) {
         double2 acc[8];
@@ -744,7 +746,12 @@ __device__ bool gram_converged(const double2* W, int m, const double* cn, double
         for (int u = 0; u < TS; ++u)
 #pragma unroll
             for (int v = 0; v < TS; ++v) acc[u][v] = make_double2(0, 0);
-        for (int k = 0; k < m; ++k) {
+        // rows visited from a lane-dependent start: the lanes of a quarter-warp
+        // read 8 different rows of their (different) columns, not one bank
+        const int k0 = threadIdx.x & 7;
+        for (int kk = 0; kk < m; ++kk) {
+            int k = kk + k0;
+            if (k >= m) k -= m;
             double2 xp[TS], xq[TS];
 #pragma unroll
             for (int u = 0; u < TS; ++u) {
