@@ -164,6 +164,34 @@ struct FrameEstimates {
     std::vector<SourceEstimate> estimates;
 };
 
+// ---- audio side (types.hpp:30-52) -----------------------------------------------
+struct SampleBlock {
+    std::uint32_t sample_rate = 16000;
+    std::vector<std::vector<float>> channels;
+    std::size_t channel_count() const { return channels.size(); }
+    std::size_t frame_count() const { return channels.empty() ? 0 : channels[0].size(); }
+    void validate() const {
+        if (channels.empty()) throw ValidationError("sample block has no channels");
+        for (const auto& c : channels)
+            if (c.size() != channels[0].size()) throw ValidationError("channels differ in length");
+    }
+};
+
+enum class WindowKind { hann, rectangular };
+
+struct StftConfig {
+    std::uint32_t frame_length = 512;
+    std::uint32_t shift = 160;
+    WindowKind window = WindowKind::hann;
+    std::uint32_t bin_min = 16;
+    std::uint32_t bin_max = 88;
+    std::uint32_t bin_count() const { return bin_max - bin_min + 1; }
+};
+
+// pipeline.hpp:56: which solver the reference runs; the device engine always
+// runs its FP64 path, so every value selects it.
+enum class SolvePath { naive, batched, reference };
+
 // ---- device contexts ---------------------------------------------------------
 class Engine {
   public:
@@ -386,6 +414,58 @@ inline std::size_t run_locate(const std::vector<SpectrumFrame>& frames, std::uin
     for (std::uint32_t b = 0; b < emitted; ++b) {
         FrameEstimates fe;
         fe.frame_index = frames[blocks[b].frame_index].frame_index;
+        for (std::uint32_t i = 0; i < blocks[b].count; ++i) {
+            const auto j = idx[std::size_t(b) * ns + i];
+            fe.estimates.push_back({j, steering.directions[j], pw[std::size_t(b) * ns + i], low[std::size_t(b) * ns + i] != 0});
+        }
+        sink(fe);
+    }
+    return emitted;
+}
+
+// run_locate with the reference's exact signature (pipeline.hpp:71-75): the
+// SampleBlock goes through the device STFT (bit-identical frames, stft.cpp:38-68)
+// straight into the correlation window.
+inline std::size_t run_locate(const SampleBlock& audio, const StftConfig& stft, std::uint32_t window_frames,
+                              const NoiseModel& noise, const SteeringField& steering, const SolverConfig& solver,
+                              const MusicConfig& music, SolvePath /*path*/, unsigned /*threads*/,
+                              const std::function<void(const FrameEstimates&)>& sink, std::uint32_t max_batch = 16) {
+    audio.validate();
+    if (window_frames == 0) throw ValidationError("window_frames must be at least 1");
+    if (noise.k.m != steering.m) throw ValidationError("noise model channel count does not match steering field");
+    if (audio.channel_count() != steering.m) throw ValidationError("sample block channel count does not match");
+    const auto m = steering.m;
+    const auto nb = std::uint32_t(steering.bin_count());
+    if (noise.k.bins.size() != stft.bin_count() || nb != stft.bin_count())
+        throw ValidationError("noise model bin count does not match the analysis band");
+    Engine e(m, nb, window_frames, music, solver, max_batch);
+    const auto kf = detail::flatten(noise.k.bins);
+    check(sslg_set_noise_model(e.get(), kf.data(), 0, nullptr));
+    const auto nd = std::uint32_t(steering.directions.size());
+    const auto d = detail::flat_dirs(steering.directions);
+    check(sslg_set_steering(e.get(), nd, reinterpret_cast<const float*>(steering.vectors.data()), d.data(), nullptr,
+                            nullptr));
+    sslg_stft_config sc{stft.frame_length, stft.shift, stft.window == WindowKind::hann ? 0 : 1, stft.bin_min,
+                        stft.bin_max};
+    check(sslg_set_stft(e.get(), &sc));
+    const std::size_t n = audio.frame_count();
+    std::vector<float> pcm;
+    pcm.reserve(m * n);
+    for (const auto& c : audio.channels) pcm.insert(pcm.end(), c.begin(), c.end());
+    std::uint32_t frames = 0;
+    check(sslg_stft(e.get(), pcm.data(), n, nullptr, 0, &frames));
+    const std::uint32_t cap = frames >= window_frames ? frames - window_frames + 1 : 0;
+    const auto ns = music.num_sources;
+    std::vector<sslg_block_out> blocks(cap ? cap : 1);
+    std::vector<std::uint32_t> idx(std::size_t(cap) * ns + 1);
+    std::vector<double> pw(std::size_t(cap) * ns + 1);
+    std::vector<std::uint8_t> low(std::size_t(cap) * ns + 1);
+    std::uint32_t emitted = 0;
+    check(sslg_locate_samples(e.get(), pcm.data(), n, cap, blocks.data(), idx.data(), pw.data(), low.data(), nullptr,
+                              &emitted));
+    for (std::uint32_t b = 0; b < emitted; ++b) {
+        FrameEstimates fe;
+        fe.frame_index = blocks[b].frame_index;
         for (std::uint32_t i = 0; i < blocks[b].count; ++i) {
             const auto j = idx[std::size_t(b) * ns + i];
             fe.estimates.push_back({j, steering.directions[j], pw[std::size_t(b) * ns + i], low[std::size_t(b) * ns + i] != 0});

@@ -114,6 +114,73 @@ int main() {
         }
         CHECK(threw);
     }
+    // pipeline.hpp:71-75 — run_locate on a SampleBlock (device STFT) gives the
+    // estimates run_locate gives on that block's STFT frames
+    {
+        const std::uint32_t m = 4, nsamp = 4000;
+        ssl::StftConfig sc;
+        sc.bin_min = 10;
+        sc.bin_max = 40;
+        ssl::SteeringField st;
+        st.m = m;
+        st.bin_min = sc.bin_min;
+        st.bin_max = sc.bin_max;
+        for (int a = 0; a < 36; ++a) st.directions.push_back({10.0 * a, 0.0});
+        const double pi = 3.14159265358979323846;
+        for (const auto& d : st.directions)
+            for (std::uint32_t b = sc.bin_min; b <= sc.bin_max; ++b)
+                for (std::uint32_t i = 0; i < m; ++i) {
+                    const double ang = 2 * pi * i / m, az = d.azimuth_deg * pi / 180;
+                    const double tau = -0.05 * (std::cos(az) * std::cos(ang) + std::sin(az) * std::sin(ang)) / 343.0;
+                    const double ph = -2 * pi * (b * 16000.0 / 512) * tau;
+                    st.vectors.push_back({float(std::cos(ph)), float(std::sin(ph))});
+                }
+        ssl::SampleBlock blk;
+        std::mt19937_64 rng(5);
+        std::normal_distribution<double> nd;
+        blk.channels.assign(m, std::vector<float>(nsamp));
+        for (std::uint32_t n = 0; n < nsamp; ++n) {
+            const double s0 = nd(rng);
+            for (std::uint32_t i = 0; i < m; ++i) blk.channels[i][n] = float(s0 + 0.3 * nd(rng));
+        }
+        const auto noise = ssl::NoiseModel::identity(m, sc.bin_count());
+        ssl::MusicConfig mc;
+        mc.num_sources = 1;
+        std::vector<ssl::FrameEstimates> a, b;
+        const auto na = ssl::run_locate(blk, sc, 8, noise, st, ssl::SolverConfig{}, mc, ssl::SolvePath::batched, 4,
+                                        [&](const ssl::FrameEstimates& fe) { a.push_back(fe); });
+        // frames of the same block through the stage entry point
+        ssl::Engine e(m, sc.bin_count(), 8, mc, ssl::SolverConfig{});
+        sslg_stft_config c{sc.frame_length, sc.shift, 0, sc.bin_min, sc.bin_max};
+        ssl::check(sslg_set_stft(e.get(), &c));
+        std::vector<float> pcm;
+        for (const auto& ch : blk.channels) pcm.insert(pcm.end(), ch.begin(), ch.end());
+        std::uint32_t nf = 0;
+        ssl::check(sslg_stft(e.get(), pcm.data(), nsamp, nullptr, 0, &nf));
+        std::vector<float> fr(std::size_t(nf) * m * sc.bin_count() * 2);
+        ssl::check(sslg_stft(e.get(), pcm.data(), nsamp, fr.data(), nf, &nf));
+        std::vector<ssl::SpectrumFrame> frames(nf);
+        for (std::uint32_t f = 0; f < nf; ++f) {
+            frames[f].frame_index = f;
+            frames[f].spectra.assign(m, std::vector<ssl::cfloat>(sc.bin_count()));
+            for (std::uint32_t i = 0; i < m; ++i)
+                for (std::uint32_t k = 0; k < sc.bin_count(); ++k) {
+                    const std::size_t o = ((std::size_t(f) * m + i) * sc.bin_count() + k) * 2;
+                    frames[f].spectra[i][k] = {fr[o], fr[o + 1]};
+                }
+        }
+        const auto nb = ssl::run_locate(frames, 8, noise, st, ssl::SolverConfig{}, mc, 4,
+                                        [&](const ssl::FrameEstimates& fe) { b.push_back(fe); });
+        CHECK(na == nb && na == nf - 7 && a.size() == b.size());
+        for (std::size_t i = 0; i < a.size() && i < b.size(); ++i) {
+            CHECK(a[i].frame_index == b[i].frame_index);
+            CHECK(a[i].estimates.size() == b[i].estimates.size());
+            for (std::size_t j = 0; j < a[i].estimates.size() && j < b[i].estimates.size(); ++j) {
+                CHECK(a[i].estimates[j].direction_index == b[i].estimates[j].direction_index);
+                CHECK(a[i].estimates[j].power == b[i].estimates[j].power);
+            }
+        }
+    }
     if (failures) {
         std::fprintf(stderr, "%d of %d checks failed\n", failures, checks);
         return 1;
