@@ -354,3 +354,30 @@ def test_correlation_window_api_semantics():
     assert np.allclose(r.bins[0], np.outer(x, x.conj()), rtol=1e-6)
     with pytest.raises(ssl.ValidationError, match="shape changed"):
         win.push(fr[:3])
+
+
+@pytest.mark.parametrize("m", [1, 17, 37, 63, 64])
+def test_generic_and_max_channel_counts_against_oracle(port, m):
+    """Channel counts outside the specialized kernels (generic m <= 64, the
+    m = 64 maximum, a single channel) against the FP64 oracle on random PSD
+    pairs of the acceptance-2 kind (acceptance.cpp:124-160): full-rank R and a
+    rank-deficient one (T < m, a vanishing block to canonicalize)."""
+    from paper_2504_03373_b200 import ssl
+
+    rng = np.random.default_rng(1000 + m)
+    bins = 3
+    kb = rng.standard_normal((bins, m, m)) + 1j * rng.standard_normal((bins, m, m))
+    k = (kb @ kb.conj().transpose(0, 2, 1) / m + 0.5 * np.eye(m)).astype(np.complex64)
+    for rank in sorted({m, max(1, m // 2)}):
+        xb = rng.standard_normal((bins, m, rank)) + 1j * rng.standard_normal((bins, m, rank))
+        r = (xb @ xb.conj().transpose(0, 2, 1) / rank).astype(np.complex64)
+        eng = ssl.Engine(m, bins, window_frames=2, max_batch=2)
+        eng.set_noise_model(k)
+        sigma, e, _, conv = eng.gsvd(r)
+        eng.close()
+        want = port.gsvd_reference(k, r, threads=4)
+        smax = want["sigma"][:, :1]
+        assert np.all(conv)
+        assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+        # vectors: compare subspaces of well-separated values and the vectors themselves
+        assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, (m, rank)
