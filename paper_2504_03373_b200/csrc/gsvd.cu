@@ -56,7 +56,8 @@ struct CanonScratch {
     unsigned ball[2];
     int dropped[kMaxM];       // columns below the final sweep's drop line
     int certcols[kMaxM];      // certified columns
-    double invd[kMaxM];       // 1 / L_jj of the CholeskyQR
+    double invd[kMaxM];       // 1 / L_jj of the CholeskyQR (column norms before it)
+    double dn2[kMaxM];        // column norms after the first projection
     int ngroups, nvanish, eligible, ndropped, ncert, collapsed;
 };
 
@@ -70,6 +71,19 @@ __device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) 
     const int t = threadIdx.x, nt = blockDim.x;
     const int nc = cs.ncert, nd = cs.ndropped;
     if (t == 0) cs.collapsed = 0;  // published by the first barrier below
+    // squared norms of the D columns (four lanes per column, nd <= 64)
+    auto dnorms = [&](double* out) {
+        const int b = t >> 2, part = t & 3;
+        double v = 0;
+        if (b < nd) {
+            const double2* wd = W + cs.dropped[b] * m;
+            for (int i = part; i < m; i += 4) v = fma(wd[i].x, wd[i].x, fma(wd[i].y, wd[i].y, v));
+        }
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        if (b < nd && part == 0) out[b] = v;
+    };
+    dnorms(cs.invd);
     for (int pass = 0; pass < 2; ++pass) {
         // G[a][b] = e_C[a]^H w_D[b], four lanes per product
         for (int e0 = 0; e0 < nc * nd; e0 += nt / 4) {
@@ -113,6 +127,15 @@ __device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) 
             *w = csub(*w, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
         }
         __syncthreads();
+        if (pass == 0) {
+            // "twice is enough" (Kahan): a second projection is needed only
+            // where the first removed more than half of a column's energy
+            dnorms(cs.dn2);
+            __syncthreads();
+            bool again = false;
+            for (int b = t; b < nd; b += nt) again |= cs.dn2[b] < 0.5 * cs.invd[b];
+            if (!__syncthreads_or(again)) break;
+        }
     }
     // D <- D L^-H with D^H D = L L^H (CholeskyQR, twice): the Q factor of D
     // in rank order, i.e. the Gram-Schmidt result; L_jj is the norm of column
