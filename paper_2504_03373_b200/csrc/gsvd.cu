@@ -449,17 +449,18 @@ __device__ long long g_qr_clk[8];
 // the serial part of every step.
 template <int MC>
 __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
-    constexpr int RP = MC > 0 ? (MC + 3) / 4 : kMaxM / 4;
+    constexpr int QL = kJacThreads / kMaxM;  // lanes per column (4 at 256 threads, 8 at 512)
+    constexpr int RP = MC > 0 ? (MC + QL - 1) / QL : kMaxM / QL;
 #ifdef SSLG_QR_TIMING
     long long _t = clock64();
 #endif
-    const int t = threadIdx.x, c = t >> 2, l = t & 3, lane = t & 31;
+    const int t = threadIdx.x, c = t / QL, l = t % QL, lane = t & 31;
     const bool own = c < m;
-    const unsigned gmask = 0xfu << (lane & ~3);
+    const unsigned gmask = ((1u << QL) - 1u) << (lane & ~(QL - 1));
     double2 y[RP];
 #pragma unroll
     for (int v = 0; v < RP; ++v) {
-        const int i = l + 4 * v;
+        const int i = l + QL * v;
         y[v] = (own && i < m) ? W[c * m + i] : make_double2(0, 0);
     }
     double nrm;  // exact squared norm of rows >= k (rows > k - 1 after the previous update)
@@ -470,8 +471,8 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
 #pragma unroll
         for (int v = 1; v < RP; v += 2) a1 = fma(y[v].x, y[v].x, fma(y[v].y, y[v].y, a1));
         nrm = a0 + a1;
-        nrm += __shfl_xor_sync(0xffffffffu, nrm, 1);
-        nrm += __shfl_xor_sync(0xffffffffu, nrm, 2);
+#pragma unroll
+        for (int o = 1; o < QL; o <<= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
         if (own && l == 0) qs.key[c] = pivot_key(nrm, c);
         if (t < kMaxM) {
             qs.u[t] = make_double2(0, 0);
@@ -489,11 +490,11 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             double2 x0 = make_double2(0, 0);
 #pragma unroll
             for (int v = 0; v < RP; ++v) {
-                const int i = l + 4 * v;
+                const int i = l + QL * v;
                 if (i == k) x0 = y[v];
                 if (i >= k && i < m) qs.u[i] = y[v];
             }
-            if (l == (k & 3)) {  // the lane that owns row k finishes the reflector
+            if (l == k % QL) {  // the lane that owns row k finishes the reflector
                 const double ax2 = fma(x0.x, x0.x, x0.y * x0.y);
                 const double alpha = fast_sqrt(nrm);
                 double2 ph = make_double2(1.0, 0.0);
@@ -520,11 +521,11 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             const double tau = act ? qs.tau : 0.0;
             // rows above k have u = 0: enter the unrolled row chunks at the
             // first active one (warp-uniform jump, no predicated-off issue)
-            const int v0 = k >> 2;
+            const int v0 = k / QL;
             double sx0 = 0, sy0 = 0, sx1 = 0, sy1 = 0;
 #define QR_DOT(v)                                                          \
     if ((v) < RP) {                                                        \
-        const double2 u = qs.u[l + 4 * (v)];                               \
+        const double2 u = qs.u[l + QL * (v)];                               \
         if ((v) & 1) {                                                     \
             sx1 = fma(u.x, y[v].x, fma(u.y, y[v].y, sx1));                 \
             sy1 = fma(u.x, y[v].y, fma(-u.y, y[v].x, sy1));                \
@@ -553,18 +554,19 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             }
 #undef QR_DOT
             double sx = sx0 + sx1, sy = sy0 + sy1;
-            sx += __shfl_xor_sync(gmask, sx, 1);
-            sy += __shfl_xor_sync(gmask, sy, 1);
-            sx += __shfl_xor_sync(gmask, sx, 2);
-            sy += __shfl_xor_sync(gmask, sy, 2);
+#pragma unroll
+            for (int o = 1; o < QL; o <<= 1) {
+                sx += __shfl_xor_sync(gmask, sx, o);
+                sy += __shfl_xor_sync(gmask, sy, o);
+            }
             const double fx = tau * sx, fy = tau * sy;
             double a0 = 0, a1 = 0;
 #define QR_UPD(v)                                                          \
     if ((v) < RP) {                                                        \
-        const double2 u = qs.u[l + 4 * (v)];                               \
+        const double2 u = qs.u[l + QL * (v)];                               \
         y[v].x -= fx * u.x - fy * u.y;                                     \
         y[v].y -= fx * u.y + fy * u.x;                                     \
-        const double e = (l + 4 * (v) > k) ? fma(y[v].x, y[v].x, y[v].y * y[v].y) : 0.0; \
+        const double e = (l + QL * (v) > k) ? fma(y[v].x, y[v].x, y[v].y * y[v].y) : 0.0; \
         if ((v) & 1) a1 += e;                                              \
         else a0 += e;                                                      \
     }
@@ -588,8 +590,8 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             }
 #undef QR_UPD
             nrm = a0 + a1;
-            nrm += __shfl_xor_sync(gmask, nrm, 1);
-            nrm += __shfl_xor_sync(gmask, nrm, 2);
+#pragma unroll
+            for (int o = 1; o < QL; o <<= 1) nrm += __shfl_xor_sync(gmask, nrm, o);
             if (act && l == 0) qs.key[c] = pivot_key(nrm, c);
         }
         QR_T(3);
@@ -598,17 +600,17 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
 #endif
         __syncthreads();
         QR_T(4);
-        if (c == p && l == (k & 3)) qs.u[k] = make_double2(0, 0);  // keep u zero above the next step
+        if (c == p && l == k % QL) qs.u[k] = make_double2(0, 0);  // keep u zero above the next step
     }
     // X = R^H: the group at pivot position j holds row j of X (conjugated
     // column j of R: rows < j in registers, beta on the diagonal); X is
     // lower triangular
-    const int bsrc = (lane & ~3) | (mypos & 3);
+    const int bsrc = (lane & ~(QL - 1)) | (mypos & (QL - 1));
     const double2 bj = make_double2(__shfl_sync(0xffffffffu, mybeta.x, bsrc), __shfl_sync(0xffffffffu, mybeta.y, bsrc));
     if (own) {
 #pragma unroll
         for (int v = 0; v < RP; ++v) {
-            const int r = l + 4 * v;
+            const int r = l + QL * v;
             if (r < m) W[r * m + mypos] = r < mypos ? cconj(y[v]) : (r == mypos ? cconj(bj) : make_double2(0, 0));
         }
     }
