@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-blocks", type=int, default=48)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--arrays", type=int, default=1,
+                   help="independent arrays (engines, one stream each) per GPU; >1 = BASELINE configs[4] (C5)")
     return p.parse_args()
 
 
@@ -254,6 +256,10 @@ def main():
 
     from paper_2504_03373_b200 import _capi, ssl
 
+    if args.arrays > 1:
+        run_arrays(args, w, rank, world, device, dist)
+        return
+
     # a dedicated stream: the engine launches on it and the CUDA events below
     # are recorded on it (torch's default stream is the legacy NULL stream)
     stream = torch.cuda.Stream(device)
@@ -437,6 +443,101 @@ def main():
         }
         print(json.dumps(line), flush=True)
     eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_arrays(args, w, rank, world, device, dist):
+    """C5 (BASELINE configs[4]): `--arrays` independent 60-ch arrays per GPU,
+    one engine context and one CUDA stream per array, all pushing `--batch`
+    new frames per step concurrently; device time from an event on a fork
+    stream to the join of every array's stream, max over ranks."""
+    import torch
+
+    from paper_2504_03373_b200 import ssl
+
+    A = args.arrays
+    main = torch.cuda.Stream(device)
+    streams = [torch.cuda.Stream(device) for _ in range(A)]
+    engines = []
+    for i in range(A):
+        e = ssl.Engine(w.m, w.bins, window_frames=w.t, music=ssl.MusicConfig(num_sources=w.ns), max_batch=args.batch,
+                       device=device, stream=streams[i].cuda_stream)
+        e.set_noise_model(w.k)
+        e.set_steering(w.h, w.dirs)
+        engines.append(e)
+    engines[0].set_stft(ssl.StftConfig(w.frame_length, w.shift, "hann", w.bin_min, w.bin_max))
+    x = engines[0].stft(w.pcm)
+    x_all = torch.from_numpy(x.view(np.float32)).to(f"cuda:{device}")
+    nfr = x_all.shape[0]
+    pos = [(17 * i) % max(1, nfr - w.t - args.batch) for i in range(A)]  # each array at its own point in the scene
+
+    def frames(i, n):
+        if pos[i] + n > nfr:
+            pos[i] = 0
+        v = x_all[pos[i]:pos[i] + n]
+        pos[i] += n
+        return v
+
+    for i, e in enumerate(engines):  # fill every window
+        left = w.t - 1
+        while left > 0:
+            nf = min(left, args.batch)
+            e.push_device(frames(i, nf).data_ptr(), nf)
+            left -= nf
+    torch.cuda.synchronize(device)
+    if dist is not None:
+        dist.barrier()
+
+    def step(timed):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(main)
+        n = 0
+        for i, e in enumerate(engines):
+            streams[i].wait_event(ev0)
+            n += e.push_device(frames(i, args.batch).data_ptr(), args.batch)
+        for i in range(A):
+            done = torch.cuda.Event()
+            done.record(streams[i])
+            main.wait_event(done)
+        ev1.record(main)
+        return ev0, ev1, n
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize(device)
+    evs, emitted = [], 0
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            a, b, n = step(True)
+            evs.append((a, b))
+            emitted += n
+        torch.cuda.synchronize(device)
+    total_ms = float(sum(a.elapsed_time(b) for a, b in evs))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=f"cuda:{device}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        e = torch.tensor([emitted], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        emitted = int(e.item())
+    value = emitted / (total_ms * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C5 (BASELINE configs[4]): {A} concurrent {w.m}-ch arrays per GPU "
+                                   f"({WORKLOADS[args.config]} scene), one engine + stream per array",
+                       "arrays_per_gpu": A, "blocks_per_step_per_array": args.batch,
+                       "parallelism": f"arrays sharded over {world} GPU(s), no data-path collective"},
+            "x_realtime_per_array": value / (A * world) / REALTIME_BLOCKS_PER_S,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    for e in engines:
+        e.close()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -31,6 +31,67 @@ __global__ void __launch_bounds__(256, 2) sweep_bench(double2* out, int m, int s
     long long t0 = clock64();
     double mymax = 0;
     int rots = 0;
+#ifdef SB_HALVE
+    int n2 = 2;
+    while (n2 < m) n2 <<= 1;
+    const bool gact = g < n2 / 2;
+    for (int sw = 0; sw < sweeps; ++sw) {
+        for (int S = n2; S >= 2; S >>= 1) {
+            const int h = S >> 1;
+            const int kset = g / h, gi = g % h;
+            const int ia = kset * S + gi;
+            int ib = kset * S + h + gi;
+            double2 Aa[kRows], Bb[kRows];
+            double ca = 0.0, cb = 0.0;
+            bool adirty = false;
+            if (gact) {
+#pragma unroll
+                for (int u = 0; u < kRows; ++u) {
+                    const int row = s + u * kLPP;
+                    Aa[u] = (row < m && ia < m) ? W[ia * m + row] : make_double2(0, 0);
+                    Bb[u] = (row < m && ib < m) ? W[ib * m + row] : make_double2(0, 0);
+                }
+                ca = ia < m ? cn[ia] : 0.0;
+                cb = ib < m ? cn[ib] : 0.0;
+            }
+            for (int rnd = 0; rnd < h; ++rnd) {
+                if (gact && ia < m && ib < m) {
+                    if (rotate_pair<kRows, kLPP>(Aa, Bb, ca, cb, 0.0, s, m, mymax)) {
+                        adirty = true;
+                        ++rots;
+#pragma unroll
+                        for (int u = 0; u < kRows; ++u) {
+                            const int row = s + u * kLPP;
+                            if (row < m) W[ib * m + row] = Bb[u];
+                        }
+                        if (s == 0) cn[ib] = cb;
+                    }
+                }
+                if (rnd + 1 < h) {
+                    __syncthreads();
+                    ib = kset * S + h + ((gi + rnd + 1) & (h - 1));
+                    if (gact) {
+#pragma unroll
+                        for (int u = 0; u < kRows; ++u) {
+                            const int row = s + u * kLPP;
+                            Bb[u] = (row < m && ib < m) ? W[ib * m + row] : make_double2(0, 0);
+                        }
+                        cb = ib < m ? cn[ib] : 0.0;
+                    }
+                }
+            }
+            if (gact && adirty) {
+#pragma unroll
+                for (int u = 0; u < kRows; ++u) {
+                    const int row = s + u * kLPP;
+                    if (row < m) W[ia * m + row] = Aa[u];
+                }
+                if (s == 0) cn[ia] = ca;
+            }
+            __syncthreads();
+        }
+    }
+#else
     for (int sw = 0; sw < sweeps; ++sw) {
         for (int r = 0; r < n_even - 1; ++r) {
             if (g < npairs) {
@@ -69,6 +130,7 @@ __global__ void __launch_bounds__(256, 2) sweep_bench(double2* out, int m, int s
             __syncthreads();
         }
     }
+#endif
     long long t1 = clock64();
     if (tid == 0) atomicAdd((unsigned long long*)clk, (unsigned long long)(t1 - t0));
     if (tid == 0) out[blockIdx.x] = make_double2(W[0].x + rots, mymax);
