@@ -301,6 +301,85 @@ __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_
     return s_ok != 0;
 }
 
+// Warp-private form of pick_fast for the concurrent canonicalization: one
+// warp per group (vanishing block or tied group), group columns s_perm[i0+k],
+// scratch G [d][d] and result Z [d][d] (coordinate k of vector t at k*d+t)
+// private to the warp; no block barrier.  Returns whether the first d
+// candidates are all accepted (else nothing usable is written).
+__device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, double2* Z, double* n0b, double* ivb,
+                               int m, int d, bool unit_norm0) {
+    const int lane = threadIdx.x & 31;
+    for (int e = lane; e < d * d; e += kWarp) {
+        const int a = e / d, b = e % d;
+        if (b < a) continue;
+        double gx = 0, gy = 0;
+        for (int k = 0; k < d; ++k) {
+            const double2 wa = W[cols[k] * m + a], wb = W[cols[k] * m + b];
+            gx = fma(wa.x, wb.x, fma(wa.y, wb.y, gx));
+            gy = fma(wa.y, wb.x, fma(-wa.x, wb.y, gy));
+        }
+        G[a * d + b] = make_double2(gx, gy);
+    }
+    __syncwarp();
+    if (lane < d) n0b[lane] = unit_norm0 ? 1.0 : sqrt(G[lane * d + lane].x);
+    __syncwarp();
+    for (int j = 0; j < d; ++j) {
+        const double gjj = G[j * d + j].x;
+        const double n0 = n0b[j];
+        const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
+        if (!(n0 > 1e-140) || !(rjj > 0.05 * n0) || !(rjj > 0)) return false;  // warp-uniform
+        const double inv = 1.0 / rjj;
+        for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
+        __syncwarp();
+        const int n = d - j - 1;
+        for (int e = lane; e < n * n; e += kWarp) {
+            const int a = j + 1 + e / n, b = j + 1 + e % n;
+            if (b < a) continue;
+            const double2 ra = G[j * d + a], rb = G[j * d + b];
+            double2& g = G[a * d + b];
+            g.x -= fma(ra.x, rb.x, ra.y * rb.y);
+            g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+        }
+        if (lane == 0) {
+            G[j * d + j] = make_double2(rjj, 0.0);
+            ivb[j] = inv;
+        }
+        __syncwarp();
+    }
+    if (lane < d) {  // Z = Y R^-1, lane = coordinate
+        const int k = lane;
+        for (int tt = 0; tt < d; ++tt) {
+            const double2 w = W[cols[k] * m + tt];
+            double2 acc = make_double2(w.x, -w.y);
+            for (int s2 = 0; s2 < tt; ++s2) acc = csub(acc, cmul(Z[k * d + s2], G[s2 * d + tt]));
+            Z[k * d + tt] = cscale(ivb[tt], acc);
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// New columns of one group from a warp-private Z: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
+__device__ void apply_span_z(double2* W, int m, int d, const int* cols, const double2* Z) {
+    const int t = threadIdx.x;
+    double2 out[6];
+    int cnt = 0;
+    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) {
+        const int i = e % m, sv = e / m;
+        double2 acc = make_double2(0, 0);
+        for (int k = 0; k < d; ++k) {
+            const double2 a = W[cols[k] * m + i], b = Z[k * d + sv];
+            acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+            acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+        }
+        out[cnt] = acc;
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) W[cols[e / m] * m + (e % m)] = out[cnt];
+    __syncthreads();
+}
+
 // Reference picker (pick_orthonormal, gsvd.cpp:404-436) on the coordinates of
 // one group: candidate j is row j of conj(N), N = W[cols[0..d)].  Threads
 // j < m own candidate j; the accepted coordinate vectors land in cs.z.
@@ -1055,19 +1134,63 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     const bool fused = cs.eligible;
     if (a.canonical && fused) {
         const int z = cs.nvanish;
-        if (z > 0) {
-            if (tid < z) cs.cols[tid] = s_perm[m - z + tid];
-            __syncthreads();
-            pick_in_span(W, Y, m, z, true, cs);
-            apply_span(W, m, z, cs);
+        // all groups (the vanishing block first, then the tied groups) are
+        // disjoint column sets: one warp each runs the QR-form picker at
+        // once, each in its own slice of the scratch (G then Z, 2 d^2
+        // entries); groups the fast path rejects, or that do not fit, take
+        // the sequential picker afterwards
+        const int ngt = cs.ngroups + (z > 0 ? 1 : 0);
+        auto grp = [&](int gi, int& i0, int& d) {
+            if (z > 0 && gi == 0) {
+                i0 = m - z;
+                d = z;
+            } else {
+                const int q = gi - (z > 0 ? 1 : 0);
+                i0 = cs.groups[q][0];
+                d = cs.groups[q][1] - i0 + 1;
+            }
+        };
+        __shared__ int s_fast[kMaxM];
+        __shared__ int s_off[kMaxM + 1];
+        if (tid == 0) {
+            int off = 0;
+            for (int gi = 0; gi < ngt; ++gi) {
+                int i0, d;
+                grp(gi, i0, d);
+                s_off[gi] = off;
+                off += 2 * d * d;
+            }
+            s_off[ngt] = off;
+        }
+        __syncthreads();
+        const bool concurrent = s_off[ngt] <= kScratch;
+        {
+            const int warp = tid / kWarp;
+            for (int gi = warp; gi < ngt; gi += kJacThreads / kWarp) {
+                int i0, d;
+                grp(gi, i0, d);
+                bool ok = false;
+                if (concurrent && d <= kZMax) {
+                    double2* G = Y + s_off[gi];
+                    ok = pick_fast_warp(W, s_perm + i0, G, G + d * d, cs.norm0 + i0, cs.nrm + i0, m, d, z > 0 && gi == 0);
+                }
+                if ((tid & 31) == 0) s_fast[gi] = ok ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        for (int gi = 0; gi < ngt; ++gi) {
+            int i0, d;
+            grp(gi, i0, d);
+            if (s_fast[gi]) apply_span_z(W, m, d, s_perm + i0, Y + s_off[gi] + d * d);
         }
         mark(7);
-        for (int gi = 0; gi < cs.ngroups; ++gi) {
-            const int i0 = cs.groups[gi][0];
-            const int d = cs.groups[gi][1] - i0 + 1;
+        for (int gi = 0; gi < ngt; ++gi) {  // after every Z slice is consumed: the scratch is free
+            int i0, d;
+            grp(gi, i0, d);
+            if (s_fast[gi]) continue;
             if (tid < d) cs.cols[tid] = s_perm[i0 + tid];
             __syncthreads();
-            pick_in_span(W, Y, m, d, false, cs);
+            pick_in_span(W, Y, m, d, z > 0 && gi == 0, cs);
             apply_span(W, m, d, cs);
         }
         // phase rule (gsvd.cpp:545-564): warp per vector
