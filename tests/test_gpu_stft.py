@@ -120,3 +120,29 @@ def test_stft_validation():
     eng.set_stft(ssl.StftConfig())
     assert eng.stft(np.zeros((2, 400), np.float32)).shape == (0, 2, 73)
     eng.close()
+
+
+def test_non_finite_samples_rejected_window_unchanged():
+    """A non-finite sample makes its frames non-finite: the push fails with the
+    reference's message (instantaneous_correlation, correlation.cpp:16-17),
+    the correlation window keeps its state, and a reset recovers the stream."""
+    from paper_2504_03373_b200.errors import ValidationError
+
+    g = np.load(GOLDEN)
+    stft = _cfg(g, "hann_band")
+    audio = g["hann_band_audio"].copy()
+    frames = g["hann_band_frames"]
+    eng = _engine(audio.shape[0], stft)
+    first = eng.push_samples(audio[:, :2000], want_power=True)
+    bad = audio[:, 2000:2400].copy()
+    bad[1, 37] = np.nan
+    with pytest.raises(ValidationError, match="non-finite"):
+        eng.push_samples(bad)
+    eng.reset_window()
+    again = eng.push_samples(audio, want_power=True)
+    ref = _engine(audio.shape[0], stft)
+    want = ref.push(frames, want_power=True)
+    assert np.array_equal(again["power"], want["power"])
+    assert first["n"] <= want["n"]
+    eng.close()
+    ref.close()
