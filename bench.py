@@ -63,6 +63,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-blocks", type=int, default=48)
     p.add_argument("--no-flush", action="store_true")
+    p.add_argument("--shard", default="arrays", choices=["arrays", "bins"],
+                   help="N>1: one array per GPU (weak) or one array's bins split over the GPUs with an all-gather "
+                        "of per-bin powers (strong, BinShardedLocator)")
     p.add_argument("--arrays", type=int, default=1,
                    help="independent arrays (engines, one stream each) per GPU; >1 = BASELINE configs[4] (C5)")
     return p.parse_args()
@@ -258,6 +261,9 @@ def main():
 
     if args.arrays > 1:
         run_arrays(args, w, rank, world, device, dist)
+        return
+    if args.shard == "bins":
+        run_bin_sharded(args, w, rank, world, device, dist)
         return
 
     # a dedicated stream: the engine launches on it and the CUDA events below
@@ -540,6 +546,71 @@ def run_arrays(args, w, rank, world, device, dist):
         e.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def run_bin_sharded(args, w, rank, world, device, dist):
+    """One array, its 257 bins split over the ranks: per push
+    every rank runs correlation + GSVD + per-bin MUSIC on its bin slice, one
+    NCCL all-gather of the per-bin powers rebuilds P[n][B][D] in bin order and
+    every rank integrates and peak-picks it (bit-identical to one GPU).  Value
+    = that array's blocks/s ("scaling": "strong")."""
+    import torch
+
+    from paper_2504_03373_b200 import ssl
+    from paper_2504_03373_b200.sharding import BinShardedLocator
+
+    if dist is None:  # single process: a one-rank group so the same code path runs
+        import torch.distributed as tdist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", device))
+        dist = tdist
+    e0 = ssl.Engine(w.m, w.bins, max_batch=args.batch, device=device)
+    e0.set_stft(ssl.StftConfig(w.frame_length, w.shift, "hann", w.bin_min, w.bin_max))
+    x = e0.stft(w.pcm)
+    e0.close()
+    loc = BinShardedLocator(w.m, w.bins, w.k, w.h, w.dirs, window_frames=w.t,
+                            music=ssl.MusicConfig(num_sources=w.ns), max_batch=args.batch, device=device)
+    pos = [0]
+
+    def frames(n):
+        if pos[0] + n > x.shape[0]:
+            pos[0] = w.t
+        v = x[pos[0]:pos[0] + n]
+        pos[0] += n
+        return v
+
+    loc.push(frames(w.t - 1))
+    for _ in range(args.warmup):
+        loc.push(frames(args.batch))
+    torch.cuda.synchronize(device)
+    dist.barrier()
+    ms, emitted = [], 0
+    with ClockSampler(device) as clk:
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(loc.stream)
+            out = loc.push(frames(args.batch))
+            b.record(loc.stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+            emitted += out["n"]
+    total = torch.tensor([float(sum(ms))], device=f"cuda:{device}")
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_ms = float(total.item())
+    value = emitted / (total_ms * 1e-3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{WORKLOADS[args.config]}: one array, bins sharded over {world} GPU(s)",
+                       "bins_per_rank": [hi - lo for lo, hi in loc.slices], "blocks_per_step": args.batch,
+                       "parallelism": f"bin-sharded x{world}, one all-gather of per-bin powers per push"},
+            "x_realtime": value / REALTIME_BLOCKS_PER_S, "clocks": clk.summary()}), flush=True)
+    dist.destroy_process_group()
 
 
 def ctypes_probe(device):
