@@ -510,12 +510,6 @@ __device__ __forceinline__ unsigned pivot_key(double n2, int c) {
 // sqrt for positive normal FP64 values (x * rsqrt(x), Newton-refined)
 __device__ __forceinline__ double fast_sqrt(double x) { return x > 0 ? x * fast_rsqrt(x) : 0.0; }
 
-#ifdef SSLG_QR_TIMING  // development harness only (tools/ubench/qr.cu)
-__device__ long long g_qr_clk[8];
-#define QR_T(i) do { if (threadIdx.x == SSLG_QR_TIMING) { long long _n = clock64(); g_qr_clk[i] += _n - _t; _t = _n; } } while (0)
-#else
-#define QR_T(i) do { } while (0)
-#endif
 
 // Column-resident QRCP: 4 lanes own one physical column of A in registers
 // (rows l, l+4, ...), so a step moves only the Householder vector through
@@ -530,9 +524,6 @@ template <int MC>
 __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
     constexpr int QL = kJacThreads / kMaxM;  // lanes per column (4 at 256 threads, 8 at 512)
     constexpr int RP = MC > 0 ? (MC + QL - 1) / QL : kMaxM / QL;
-#ifdef SSLG_QR_TIMING
-    long long _t = clock64();
-#endif
     const int t = threadIdx.x, c = t / QL, l = t % QL, lane = t & 31;
     const bool own = c < m;
     const unsigned gmask = ((1u << QL) - 1u) << (lane & ~(QL - 1));
@@ -564,7 +555,6 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
     for (int k = 0; k < m; ++k) {
         const unsigned kk = __reduce_max_sync(0xffffffffu, max(qs.key[lane], qs.key[lane + 32]));
         const int p = 63 - (int)((kk - 1u) & 63u);
-        QR_T(0);
         if (c == p) {
             double2 x0 = make_double2(0, 0);
 #pragma unroll
@@ -591,9 +581,7 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             }
             mypos = k;
         }
-        QR_T(1);
         __syncthreads();
-        QR_T(2);
         {  // every group runs the update (no divergence around the group
            // shuffles); pivoted and padding groups apply a zero multiple
             const bool act = own && mypos < 0;
@@ -673,12 +661,7 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             for (int o = 1; o < QL; o <<= 1) nrm += __shfl_xor_sync(gmask, nrm, o);
             if (act && l == 0) qs.key[c] = pivot_key(nrm, c);
         }
-        QR_T(3);
-#ifdef SSLG_QR_TIMING
-        if (threadIdx.x == SSLG_QR_TIMING) { g_qr_clk[5] = mypos; g_qr_clk[6] += (own && mypos < 0); }
-#endif
         __syncthreads();
-        QR_T(4);
         if (c == p && l == k % QL) qs.u[k] = make_double2(0, 0);  // keep u zero above the next step
     }
     // X = R^H: the group at pivot position j holds row j of X (conjugated

@@ -1,8 +1,5 @@
 // Standalone latency harness for the QRCP phase (development aid): one CTA,
-// random 60x60 complex matrix, clock64 per sub-phase for a chosen thread.
-#ifndef SSLG_QR_TIMING
-#define SSLG_QR_TIMING 0
-#endif
+// random 60x60 complex matrix, clock64 around the factorization.
 #include "../../paper_2504_03373_b200/csrc/gsvd.cu"
 #include <cstdio>
 #include <cstdlib>
@@ -29,13 +26,9 @@ int main() {
     cudaMemcpy(a, h, sizeof h, cudaMemcpyHostToDevice);
     cudaFuncSetAttribute(qr_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 60000);
     for (int r = 0; r < 2; ++r) {
-        long long z[8] = {0};
-        cudaMemcpyToSymbol(g_qr_clk, z, sizeof z);
         qr_bench<<<1, 256, 60000>>>(a, o, clk, m);
         cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
-        cudaMemcpyFromSymbol(z, g_qr_clk, sizeof z);
-        printf("qrcp_to_rh<60>: %lld cycles (%s); thread %d: argmax %lld pivot %lld bar1 %lld update %lld bar2 %lld mypos %lld nupd %lld\n", c,
-               cudaGetErrorString(cudaGetLastError()), SSLG_QR_TIMING, z[0], z[1], z[2], z[3], z[4], z[5], z[6]);
+        printf("qrcp_to_rh<60>: %lld cycles (%s)\n", c, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }
