@@ -586,40 +586,34 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
            // shuffles); pivoted and padding groups apply a zero multiple
             const bool act = own && mypos < 0;
             const double tau = act ? qs.tau : 0.0;
-            // rows above k have u = 0: enter the unrolled row chunks at the
-            // first active one (warp-uniform jump, no predicated-off issue)
+            // rows above k have u = 0, so whole segments of 3 row chunks below
+            // the first active chunk are skipped (warp-uniform) and the rest
+            // run unpredicated; a segment issues its 3 Householder loads
+            // before its FMAs, keeping them in flight together
             const int v0 = k / QL;
+            constexpr int SEG = 3;
             double sx0 = 0, sy0 = 0, sx1 = 0, sy1 = 0;
-#define QR_DOT(v)                                                          \
-    if ((v) < RP) {                                                        \
-        const double2 u = qs.u[l + QL * (v)];                               \
-        if ((v) & 1) {                                                     \
-            sx1 = fma(u.x, y[v].x, fma(u.y, y[v].y, sx1));                 \
-            sy1 = fma(u.x, y[v].y, fma(-u.y, y[v].x, sy1));                \
-        } else {                                                           \
-            sx0 = fma(u.x, y[v].x, fma(u.y, y[v].y, sx0));                 \
-            sy0 = fma(u.x, y[v].y, fma(-u.y, y[v].x, sy0));                \
-        }                                                                  \
-    }
-            switch (v0) {
-                case 0: QR_DOT(0) [[fallthrough]];
-                case 1: QR_DOT(1) [[fallthrough]];
-                case 2: QR_DOT(2) [[fallthrough]];
-                case 3: QR_DOT(3) [[fallthrough]];
-                case 4: QR_DOT(4) [[fallthrough]];
-                case 5: QR_DOT(5) [[fallthrough]];
-                case 6: QR_DOT(6) [[fallthrough]];
-                case 7: QR_DOT(7) [[fallthrough]];
-                case 8: QR_DOT(8) [[fallthrough]];
-                case 9: QR_DOT(9) [[fallthrough]];
-                case 10: QR_DOT(10) [[fallthrough]];
-                case 11: QR_DOT(11) [[fallthrough]];
-                case 12: QR_DOT(12) [[fallthrough]];
-                case 13: QR_DOT(13) [[fallthrough]];
-                case 14: QR_DOT(14) [[fallthrough]];
-                default: QR_DOT(15)
+#pragma unroll
+            for (int s0 = 0; s0 < RP; s0 += SEG) {
+                if (v0 <= s0 + SEG - 1) {
+                    double2 uu[SEG];
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) uu[j] = s0 + j < RP ? qs.u[l + QL * (s0 + j)] : make_double2(0, 0);
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) {
+                        const int v = s0 + j;
+                        if (v < RP) {
+                            if (v & 1) {
+                                sx1 = fma(uu[j].x, y[v].x, fma(uu[j].y, y[v].y, sx1));
+                                sy1 = fma(uu[j].x, y[v].y, fma(-uu[j].y, y[v].x, sy1));
+                            } else {
+                                sx0 = fma(uu[j].x, y[v].x, fma(uu[j].y, y[v].y, sx0));
+                                sy0 = fma(uu[j].x, y[v].y, fma(-uu[j].y, y[v].x, sy0));
+                            }
+                        }
+                    }
+                }
             }
-#undef QR_DOT
             double sx = sx0 + sx1, sy = sy0 + sy1;
 #pragma unroll
             for (int o = 1; o < QL; o <<= 1) {
@@ -628,34 +622,25 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
             }
             const double fx = tau * sx, fy = tau * sy;
             double a0 = 0, a1 = 0;
-#define QR_UPD(v)                                                          \
-    if ((v) < RP) {                                                        \
-        const double2 u = qs.u[l + QL * (v)];                               \
-        y[v].x -= fx * u.x - fy * u.y;                                     \
-        y[v].y -= fx * u.y + fy * u.x;                                     \
-        const double e = (l + QL * (v) > k) ? fma(y[v].x, y[v].x, y[v].y * y[v].y) : 0.0; \
-        if ((v) & 1) a1 += e;                                              \
-        else a0 += e;                                                      \
-    }
-            switch (v0) {
-                case 0: QR_UPD(0) [[fallthrough]];
-                case 1: QR_UPD(1) [[fallthrough]];
-                case 2: QR_UPD(2) [[fallthrough]];
-                case 3: QR_UPD(3) [[fallthrough]];
-                case 4: QR_UPD(4) [[fallthrough]];
-                case 5: QR_UPD(5) [[fallthrough]];
-                case 6: QR_UPD(6) [[fallthrough]];
-                case 7: QR_UPD(7) [[fallthrough]];
-                case 8: QR_UPD(8) [[fallthrough]];
-                case 9: QR_UPD(9) [[fallthrough]];
-                case 10: QR_UPD(10) [[fallthrough]];
-                case 11: QR_UPD(11) [[fallthrough]];
-                case 12: QR_UPD(12) [[fallthrough]];
-                case 13: QR_UPD(13) [[fallthrough]];
-                case 14: QR_UPD(14) [[fallthrough]];
-                default: QR_UPD(15)
+#pragma unroll
+            for (int s0 = 0; s0 < RP; s0 += SEG) {
+                if (v0 <= s0 + SEG - 1) {
+                    double2 uu[SEG];
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) uu[j] = s0 + j < RP ? qs.u[l + QL * (s0 + j)] : make_double2(0, 0);
+#pragma unroll
+                    for (int j = 0; j < SEG; ++j) {
+                        const int v = s0 + j;
+                        if (v < RP) {
+                            y[v].x = fma(-fx, uu[j].x, fma(fy, uu[j].y, y[v].x));
+                            y[v].y = fma(-fx, uu[j].y, fma(-fy, uu[j].x, y[v].y));
+                            const double e = (l + QL * v > k) ? fma(y[v].x, y[v].x, y[v].y * y[v].y) : 0.0;
+                            if (v & 1) a1 += e;
+                            else a0 += e;
+                        }
+                    }
+                }
             }
-#undef QR_UPD
             nrm = a0 + a1;
 #pragma unroll
             for (int o = 1; o < QL; o <<= 1) nrm += __shfl_xor_sync(gmask, nrm, o);
