@@ -67,7 +67,9 @@ struct CanonScratch {
 // scratch G, |C||D| <= m^2/4 entries), then one warp runs two classical
 // Gram-Schmidt passes per column of D against the earlier ones (8 dots per
 // butterfly) and normalizes it.  Clears cs.eligible if a column collapses.
-__device__ void complete_basis(double2* W, double2* G, int m, CanonScratch& cs) {
+template <int MC>
+__device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& cs) {
+    const int m = MC > 0 ? MC : m_rt;
     const int t = threadIdx.x, nt = blockDim.x;
     const int nc = cs.ncert, nd = cs.ndropped;
     if (t == 0) cs.collapsed = 0;  // published by the first barrier below
@@ -306,8 +308,10 @@ __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_
 // scratch G [d][d] and result Z [d][d] (coordinate k of vector t at k*d+t)
 // private to the warp; no block barrier.  Returns whether the first d
 // candidates are all accepted (else nothing usable is written).
+template <int MC>
 __device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, double2* Z, double* n0b, double* ivb,
-                               int m, int d, bool unit_norm0) {
+                               int m_rt, int d, bool unit_norm0) {
+    const int m = MC > 0 ? MC : m_rt;
     const int lane = threadIdx.x & 31;
     for (int e = lane; e < d * d; e += kWarp) {
         const int a = e / d, b = e % d;
@@ -360,7 +364,9 @@ __device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, do
 }
 
 // New columns of one group from a warp-private Z: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
-__device__ void apply_span_z(double2* W, int m, int d, const int* cols, const double2* Z) {
+template <int MC>
+__device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const double2* Z) {
+    const int m = MC > 0 ? MC : m_rt;
     const int t = threadIdx.x;
     double2 out[6];
     int cnt = 0;
@@ -801,7 +807,9 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
 // iff the next sweep would rotate nothing (gsvd.cpp:642-649).  Evaluated as
 // one 4x4-register-tiled Gram product over the upper triangle instead of a
 // full verification sweep of round-synchronized pair visits.
-__device__ bool gram_converged(const double2* W, int m, const double* cn, double drop) {
+template <int MC>
+__device__ bool gram_converged(const double2* W, int m_rt, const double* cn, double drop) {
+    const int m = MC > 0 ? MC : m_rt;
     constexpr int TS = 2;  // 2x2 tiles keep the kernel's register budget
     const int nt = (m + TS - 1) / TS;
     const int ntiles = nt * (nt + 1) / 2;
@@ -944,7 +952,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         // <= 1e-8 relative (whose rotations leave couplings ~1e-16, squared
         // far below the 1e-28 test), is usually rotation-free: certify that
         // with one Gram product instead of running it.
-        if (sweep > 0 && (16 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged(W, m, cn, drop)) {
+        if (sweep > 0 && (16 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC>(W, m, cn, drop)) {
             converged = true;
             break;
         }
@@ -1097,7 +1105,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     __syncthreads();
     // the preconditioned vectors are re-orthonormalized whichever kernel
     // canonicalizes them (the generic one reads the lead vectors too)
-    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis(W, Y, m, cs);
+    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis<MC>(W, Y, m, cs);
     mark(4);
     const bool fused = cs.eligible;
     if (a.canonical && fused) {
@@ -1140,7 +1148,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
                 bool ok = false;
                 if (concurrent && d <= kZMax) {
                     double2* G = Y + s_off[gi];
-                    ok = pick_fast_warp(W, s_perm + i0, G, G + d * d, cs.norm0 + i0, cs.nrm + i0, m, d, z > 0 && gi == 0);
+                    ok = pick_fast_warp<MC>(W, s_perm + i0, G, G + d * d, cs.norm0 + i0, cs.nrm + i0, m, d, z > 0 && gi == 0);
                 }
                 if ((tid & 31) == 0) s_fast[gi] = ok ? 1 : 0;
             }
@@ -1149,7 +1157,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         for (int gi = 0; gi < ngt; ++gi) {
             int i0, d;
             grp(gi, i0, d);
-            if (s_fast[gi]) apply_span_z(W, m, d, s_perm + i0, Y + s_off[gi] + d * d);
+            if (s_fast[gi]) apply_span_z<MC>(W, m, d, s_perm + i0, Y + s_off[gi] + d * d);
         }
         mark(7);
         for (int gi = 0; gi < ngt; ++gi) {  // after every Z slice is consumed: the scratch is free
