@@ -185,14 +185,15 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& c
                     gij = cscale(inv, gij);
                 }
                 __syncwarp();
-                for (int i = j + 1 + t; i < nd; i += kWarp) {
-                    const double2 lij = G[i * (i + 1) / 2 + j];
-                    for (int k = j + 1; k <= i; ++k) {
-                        const double2 lkj = G[k * (k + 1) / 2 + j];
-                        double2& gik = G[i * (i + 1) / 2 + k];
-                        gik.x -= fma(lij.x, lkj.x, lij.y * lkj.y);
-                        gik.y -= fma(lij.y, lkj.x, -lij.x * lkj.y);
-                    }
+                // trailing lower triangle, one (i, k) entry per lane at a time
+                const int n = nd - j - 1;
+                for (int e = t; e < n * n; e += kWarp) {
+                    const int i = j + 1 + e / n, k = j + 1 + e % n;
+                    if (k > i) continue;
+                    const double2 lij = G[i * (i + 1) / 2 + j], lkj = G[k * (k + 1) / 2 + j];
+                    double2& gik = G[i * (i + 1) / 2 + k];
+                    gik.x -= fma(lij.x, lkj.x, lij.y * lkj.y);
+                    gik.y -= fma(lij.y, lkj.x, -lij.x * lkj.y);
                 }
                 if (t == 0) invd[j] = inv;
                 __syncwarp();
