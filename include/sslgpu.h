@@ -190,6 +190,22 @@ int sslg_locate_samples(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint
                         sslg_block_out* blocks, uint32_t* est_idx, double* est_power, uint8_t* est_low,
                         double* power, uint32_t* emitted);
 
+/* ---- asynchronous streaming -------------------------------------------------
+ * sslg_push_samples_async enqueues a push (H2D of the PCM, device STFT, a
+ * device-side non-finite gate, the hot path, D2H of the estimates into a
+ * pinned result ring) on the context stream and returns without waiting; any
+ * number of pushes may be in flight (up to 16 max_batch chunks uncollected).
+ * `pcm` must stay valid until the push is collected; pinned (cudaHostAlloc)
+ * memory lets the copy overlap the previous push's kernels.  *ticket marks
+ * the end of this call's results.  sslg_wait_results waits for every push up
+ * to `ticket` and copies their blocks out in order.  A non-finite value stops
+ * the stream on the device (later pushes skip their kernels), the window is
+ * rewound to just before the failing push and SSLG_VALIDATION is returned;
+ * sslg_reset_window restarts the stream. */
+int sslg_push_samples_async(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint64_t* ticket);
+int sslg_wait_results(sslg_ctx* ctx, uint64_t ticket, uint32_t cap_blocks, sslg_block_out* blocks, uint32_t* est_idx,
+                      double* est_power, uint8_t* est_low, double* power, uint32_t* emitted);
+
 /* ---- stage entry points (host buffers, one call per reference function) */
 
 /* CorrelationWindow push + normalized (correlation.cpp:86-130) for nframes

@@ -96,6 +96,9 @@ EXPORTS = {
                                     _u8p, _f64p, _u32p]),
     "sslg_locate_samples": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, C.c_uint32, C.POINTER(BlockOut), _u32p,
                                       _f64p, _u8p, _f64p, _u32p]),
+    "sslg_push_samples_async": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "sslg_wait_results": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.POINTER(BlockOut), _u32p, _f64p, _u8p,
+                                    _f64p, _u32p]),
 }
 
 _lib = None

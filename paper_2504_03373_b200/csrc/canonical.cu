@@ -167,6 +167,7 @@ __device__ void pick_right_looking(double2* cand, int m, int need, double2* out,
 }
 
 __global__ void __launch_bounds__(kCanThreads, 1) canonical_kernel(CanonArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = a.m;
     const int mm = m * m;

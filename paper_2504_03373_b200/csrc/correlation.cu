@@ -40,6 +40,7 @@ __device__ __forceinline__ void outer_acc(double2& acc, float2 xi, float2 xj, bo
 }
 
 __global__ void __launch_bounds__(kCorrThreads) correlation_kernel(CorrArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     __shared__ float2 xs_new[kMaxM];
     __shared__ float2 xs_old[kMaxM];
     const int b = blockIdx.x;
@@ -121,6 +122,22 @@ __global__ void count_nonfinite_kernel(const float* p, size_t n, unsigned int* b
     unsigned int local = 0;
     for (; i < n; i += stride) local += isfinite(p[i]) ? 0u : 1u;
     if (local) atomicAdd(bad, local);
+}
+
+__global__ void gate_abort_kernel(const float* p, size_t n, unsigned int* abort, unsigned int id) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (; i < n; i += stride) bad |= !isfinite(p[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(abort, 0u, id + 1u);
+}
+
+void launch_gate_abort(const float* p, size_t n, unsigned int* abort, unsigned int id, cudaStream_t s) {
+    const int threads = 256;
+    size_t blocks = (n + threads - 1) / threads;
+    if (blocks > 1024) blocks = 1024;
+    if (blocks == 0) blocks = 1;
+    gate_abort_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, n, abort, id);
 }
 
 void launch_correlation(const CorrArgs& a, cudaStream_t s) {

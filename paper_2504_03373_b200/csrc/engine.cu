@@ -129,6 +129,27 @@ struct sslg_ctx {
     size_t samp_fill = 0;          // samples held in samp[samp_cur]
     int samp_cur = 0;
     float2* frame_scratch = nullptr;  // [max_batch][m][bins] for the stage entry point
+    // asynchronous streaming (sslg_push_samples_async / sslg_wait_results)
+    unsigned int* abort = nullptr;  // device word: 0, or 1 + id of the first sub-push whose gate failed
+    struct Slot {
+        cudaEvent_t done = nullptr;
+        uint32_t* idx = nullptr;   // pinned [max_batch][ns]
+        double* pw = nullptr;      // pinned [max_batch][ns]
+        uint8_t* low = nullptr;    // pinned [max_batch][ns]
+        uint32_t* cnt = nullptr;   // pinned [max_batch]
+        double* power = nullptr;   // pinned [max_batch][dirs] (allocated with the steering)
+        uint32_t n = 0;
+        long long first_frame = 0;
+        long long pushed0 = 0, since0 = 0;  // window counters before this sub-push
+        uint64_t id = 0;
+        bool pending = false;
+    };
+    static constexpr int kSlots = 16;
+    Slot slots[kSlots];
+    uint64_t next_id = 0;       // sub-pushes enqueued
+    uint64_t collected = 0;     // sub-pushes handed back by sslg_wait_results
+    bool poisoned = false;
+    uint32_t poison_code = 0;
 };
 
 namespace {
@@ -175,12 +196,14 @@ int run_gsvd(sslg_ctx* c, int n) {
     GsvdArgs ga{c->r,   c->kinv, c->sigma, c->e, c->sweeps, c->conv, c->work, (int)g.m, (int)g.bins,
                 g.max_sweeps ? (int)g.max_sweeps : 60, g.canonical_subspaces, g.refine_leading,
                 g.precondition, c->ascratch, c->phase_clk};
+    ga.abort = c->abort;
     launch_jacobi(ga, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
     if (g.canonical_subspaces) {
         CanonArgs ca{c->r, c->kinv, c->sigma, c->e, c->work, (int)g.m, (int)g.bins, g.refine_leading};
+        ca.abort = c->abort;
         launch_canonical(ca, n, c->stream);
         ++c->launches;
         TRY(check_last_launch("canonical_kernel"));
@@ -193,12 +216,14 @@ int run_music(sslg_ctx* c, int n) {
     const sslg_config& g = c->cfg;
     SpecArgs sa{c->e, c->h_t, c->num, c->p, (int)g.m, (int)g.bins, (int)c->dirs, (int)g.num_sources, 0, 0,
                 (double)g.denominator_floor, g.squared_denominator};
+    sa.abort = c->abort;
     launch_spectrum(sa, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("spectrum_kernel"));
     CU(cudaEventRecord(c->ev[4], c->stream));
     PeakArgs pa{c->p, c->power, c->nbr_off, c->nbr, c->est_idx, c->est_pw, c->est_low, c->est_count,
                 (int)g.bins, (int)c->dirs, (int)g.num_sources, (double)g.low_power_ratio};
+    pa.abort = c->abort;
     launch_peaks(pa, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("integrate_peaks_kernel"));
@@ -254,6 +279,7 @@ int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
     CU(cudaEventRecord(c->ev[0], c->stream));
     CorrArgs ca{c->ring, c->state, c->r, (int)g.m, (int)g.bins, (int)g.window_frames, c->cap, (int)nframes,
                 c->pushed, c->since, (int)(g.rebuild_interval ? g.rebuild_interval : 1)};
+    ca.abort = c->abort;
     launch_correlation(ca, c->stream);
     ++c->launches;
     TRY(check_last_launch("correlation_kernel"));
@@ -282,6 +308,7 @@ int require_ready(sslg_ctx* c) {
     if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
     if (c->cfg.num_sources >= c->cfg.m)
         return set_err(SSLG_VALIDATION, "num_sources must be smaller than the channel count");
+    if (c->poisoned) return set_err(SSLG_VALIDATION, "stream stopped by a non-finite spectrum value; reset the window");
     CU(cudaSetDevice(c->cfg.device));
     return 0;
 }
@@ -361,6 +388,18 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     }
     rc |= dalloc(&c->est_count, NB);
     rc |= dalloc(&c->flags, 8);
+    rc |= dalloc(&c->abort, 1);
+    if (!rc && cudaMemsetAsync(c->abort, 0, sizeof(unsigned int), c->stream) != cudaSuccess)
+        rc = set_err(SSLG_DEVICE, "cudaMemset failed");
+    for (auto& sl : c->slots) {
+        if (rc) break;
+        if (cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess ||
+            cudaMallocHost(&sl.idx, NB * g.num_sources * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMallocHost(&sl.pw, NB * g.num_sources * sizeof(double)) != cudaSuccess ||
+            cudaMallocHost(&sl.low, NB * g.num_sources) != cudaSuccess ||
+            cudaMallocHost(&sl.cnt, NB * sizeof(uint32_t)) != cudaSuccess)
+            rc = set_err(SSLG_DEVICE, "pinned result ring allocation failed");
+    }
     for (int i = 0; i < 6 && !rc; ++i)
         if (cudaEventCreate(&c->ev[i]) != cudaSuccess) rc = set_err(SSLG_DEVICE, "cudaEventCreate failed");
     if (!rc && cudaMemsetAsync(c->state, 0, B * mm * sizeof(double2), c->stream) != cudaSuccess)
@@ -383,8 +422,14 @@ void sslg_destroy(sslg_ctx* c) {
                     c->flags};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch})
+    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch,
+                    (void*)c->abort})
         if (p) cudaFree(p);
+    for (auto& sl : c->slots) {
+        for (void* p : {(void*)sl.idx, (void*)sl.pw, (void*)sl.low, (void*)sl.cnt, (void*)sl.power})
+            if (p) cudaFreeHost(p);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -526,6 +571,11 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
         TRY(dalloc(&c->est_idx, NB * g.num_sources));
         TRY(dalloc(&c->est_pw, NB * g.num_sources));
         TRY(dalloc(&c->est_low, NB * g.num_sources));
+        for (auto& sl : c->slots) {
+            if (sl.power) cudaFreeHost(sl.power);
+            sl.power = nullptr;
+            CU(cudaMallocHost(&sl.power, NB * dirs * sizeof(double)));
+        }
         c->dirs = dirs;
     }
     if (c->nbr_off) cudaFree(c->nbr_off);
@@ -552,6 +602,12 @@ int sslg_reset_window(sslg_ctx* c) {
     c->since = 0;
     c->last_emitted = 0;
     c->samp_fill = 0;
+    // asynchronous pushes in flight are discarded
+    CU(cudaMemsetAsync(c->abort, 0, sizeof(unsigned int), c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    for (auto& sl : c->slots) sl.pending = false;
+    c->collected = c->next_id;
+    c->poisoned = false;
     return SSLG_OK;
 }
 
@@ -993,6 +1049,113 @@ int sslg_locate_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32
     TRY(sslg_reset_window(c));
     c->samp_fill = 0;
     return sslg_push_samples(c, pcm, nsamples, cap_blocks, blocks, est_idx, est_power, est_low, power, emitted);
+}
+
+// ---- asynchronous streaming --------------------------------
+
+int sslg_push_samples_async(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint64_t* ticket) {
+    TRY(require_ready(c));
+    if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
+    if (!pcm && nsamples) return set_err(SSLG_VALIDATION, "null argument");
+    if (c->poisoned) return set_err(SSLG_VALIDATION, "stream stopped by a non-finite spectrum value; reset the window");
+    uint32_t frames = 0;
+    TRY(sslg_samples_pending(c, nsamples, &frames, nullptr));
+    const uint32_t subs = (frames + c->cfg.max_batch - 1) / c->cfg.max_batch;
+    if (c->next_id - c->collected + subs > (uint64_t)sslg_ctx::kSlots)
+        return set_err(SSLG_VALIDATION, "asynchronous result ring full; collect results with sslg_wait_results");
+    const sslg_config& g = c->cfg;
+    const size_t ns = g.num_sources;
+    uint64_t off = 0;
+    for (;;) {
+        size_t took = 0;
+        TRY(append_samples(c, pcm + off, nsamples, nsamples - off, &took));
+        off += took;
+        const uint32_t nf = frames_ready(c);
+        if (nf == 0) {
+            if (off >= nsamples) break;
+            continue;
+        }
+        auto& sl = c->slots[c->next_id % sslg_ctx::kSlots];
+        sl.id = c->next_id;
+        sl.pushed0 = c->pushed;
+        sl.since0 = c->since;
+        c->launches = 0;
+        TRY(launch_stft_frames(c, c->samp[c->samp_cur], c->samp_cap, (int)nf, c->ring, c->cap, c->pushed));
+        // device-side gate: the first failing sub-push stops everything after it
+        const size_t fsz = (size_t)g.m * g.bins;
+        for (uint32_t done = 0; done < nf;) {
+            const int slot = (int)((c->pushed + done) % c->cap);
+            const uint32_t run = std::min<uint32_t>(nf - done, (uint32_t)(c->cap - slot));
+            launch_gate_abort(reinterpret_cast<const float*>(c->ring + (size_t)slot * fsz), run * fsz * 2, c->abort,
+                              (unsigned)sl.id, c->stream);
+            done += run;
+        }
+        uint32_t e = 0;
+        TRY(process_chunk(c, nf, &e));
+        TRY(consume_samples(c, (size_t)nf * c->stft.shift));
+        sl.n = e;
+        sl.first_frame = c->last_first_frame;
+        if (e) {
+            CU(cudaMemcpyAsync(sl.idx, c->est_idx, e * ns * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(sl.pw, c->est_pw, e * ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(sl.low, c->est_low, e * ns, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(sl.cnt, c->est_count, e * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(sl.power, c->power, (size_t)e * c->dirs * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+        }
+        CU(cudaEventRecord(sl.done, c->stream));
+        sl.pending = true;
+        ++c->next_id;
+    }
+    if (ticket) *ticket = c->next_id;  // every sub-push before this id belongs to the call
+    return SSLG_OK;
+}
+
+int sslg_wait_results(sslg_ctx* c, uint64_t ticket, uint32_t cap_blocks, sslg_block_out* blocks, uint32_t* est_idx,
+                      double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
+    if (emitted) *emitted = 0;
+    if (c->poisoned) return set_err(SSLG_VALIDATION, "non-finite spectrum value");
+    if (ticket > c->next_id) return set_err(SSLG_VALIDATION, "unknown ticket");
+    const size_t ns = c->cfg.num_sources, D = c->dirs;
+    // wait for the last requested sub-push, then check the abort word once
+    if (ticket > c->collected) CU(cudaEventSynchronize(c->slots[(ticket - 1) % sslg_ctx::kSlots].done));
+    unsigned int ab = 0;
+    CU(cudaMemcpy(&ab, c->abort, sizeof ab, cudaMemcpyDeviceToHost));
+    uint32_t out = 0;
+    while (c->collected < ticket) {
+        auto& sl = c->slots[c->collected % sslg_ctx::kSlots];
+        if (ab && sl.id + 1 >= ab) {
+            // this sub-push's gate (or an earlier one of this stream) failed:
+            // nothing from here on touched the window; rewind to it
+            c->pushed = sl.pushed0;
+            c->since = sl.since0;
+            c->samp_fill = 0;
+            c->poisoned = true;
+            for (auto& s2 : c->slots) s2.pending = false;
+            c->collected = c->next_id;
+            CU(cudaMemsetAsync(c->abort, 0, sizeof(unsigned int), c->stream));
+            if (emitted) *emitted = out;
+            return set_err(SSLG_VALIDATION, "non-finite spectrum value");
+        }
+        if (out + sl.n > cap_blocks) return set_err(SSLG_VALIDATION, "result arrays too small for the emitted blocks");
+        for (uint32_t b = 0; b < sl.n; ++b) {
+            if (blocks) {
+                blocks[out + b].frame_index = (uint32_t)(sl.first_frame + b);
+                blocks[out + b].count = sl.cnt[b];
+            }
+        }
+        if (est_idx) std::memcpy(est_idx + out * ns, sl.idx, sl.n * ns * sizeof(uint32_t));
+        if (est_power) std::memcpy(est_power + out * ns, sl.pw, sl.n * ns * sizeof(double));
+        if (est_low) std::memcpy(est_low + out * ns, sl.low, sl.n * ns);
+        if (power) std::memcpy(power + (size_t)out * D, sl.power, (size_t)sl.n * D * sizeof(double));
+        out += sl.n;
+        sl.pending = false;
+        ++c->collected;
+    }
+    if (emitted) *emitted = out;
+    return SSLG_OK;
 }
 
 }  // extern "C"

@@ -865,6 +865,7 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
 // addressing fold away); MC == 0: any m <= 64 at run time.
 template <int MC>
 __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = MC > 0 ? MC : a.m;
     double2* W = reinterpret_cast<double2*>(smem_raw);  // [m cols][m rows]

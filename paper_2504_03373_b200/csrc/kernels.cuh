@@ -27,9 +27,12 @@ struct CorrArgs {
     long long pushed0;   // pushes before this launch (== global index of first frame)
     long long since0;    // pushes since the last rebuild
     int rebuild_interval;
+    const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_correlation(const CorrArgs& a, cudaStream_t s);
 void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStream_t s);
+// async gate: the first failing push id + 1 lands in *abort (atomicCAS from 0)
+void launch_gate_abort(const float* p, size_t n, unsigned int* abort, unsigned int id, cudaStream_t s);
 
 void launch_gauss_jordan(const float2* k, int m, int bins, double2* inv_out, unsigned int* bad_f,
                          unsigned int* bad_d, cudaStream_t s);
@@ -49,6 +52,7 @@ struct GsvdArgs {
     int precondition;     // QR-preconditioned Jacobi (needs ascratch)
     double2* ascratch;    // [nblk][bins][m][m] column-major copy of A (precondition)
     long long* phase_clk; // optional [8] summed SM clocks per solver phase (diagnostics)
+    const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 
@@ -59,6 +63,7 @@ struct CanonArgs {
     double2* e;              // [nblk][bins][m vec][m row]  (in/out)
     uint32_t* work;          // worklist filled by jacobi_kernel (see GsvdArgs)
     int m, bins, refine;
+    const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_canonical(const CanonArgs& a, int nblk, cudaStream_t s);
 
@@ -70,6 +75,7 @@ struct SpecArgs {
     int m, bins, dirs, ns, dchunk, nsplit;
     double floor_;
     int squared;
+    const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s);
 void launch_steering_prep(const float2* h_in, float2* h_t, double* num, int m, int bins, int dirs,
@@ -86,6 +92,7 @@ struct PeakArgs {
     uint32_t* est_count;      // [nblk]
     int bins, dirs, ns;
     double low_ratio;         // double(float ratio)
+    const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_peaks(const PeakArgs& a, int nblk, cudaStream_t s);
 

@@ -24,6 +24,7 @@ constexpr int kSpecThreads = 256;
 constexpr int kSpecVec = 4;  // noise vectors per steering load
 
 __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = a.m;
     const int nn = m - a.ns;
@@ -97,6 +98,7 @@ constexpr int kEStride = kNPad + 1;          // double2 row stride of the staged
 constexpr int kHStride = kChunk2 + 2;        // float2 row stride of the staged steering (16-B aligned rows)
 
 __global__ void __launch_bounds__(256, 2) spectrum_tiled_kernel(SpecArgs a, int nblk, int nchunk) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = a.m;
     const int nn = m - a.ns;
@@ -203,6 +205,7 @@ __global__ void steering_prep_kernel(const float2* __restrict__ h_in,  // [dirs]
 constexpr int kPeakThreads = 256;
 
 __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* pw = reinterpret_cast<double*>(smem_raw);              // [dirs]
     int* is_peak = reinterpret_cast<int*>(pw + a.dirs);            // [dirs]

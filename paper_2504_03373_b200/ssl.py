@@ -379,6 +379,38 @@ class Engine:
         """run_locate over one SampleBlock (pipeline.cpp:210-247): fresh window."""
         return self._samples_call(self.L.sslg_locate_samples, pcm, want_power)
 
+    def push_samples_async(self, pcm: np.ndarray) -> int:
+        """Enqueues a streaming push without waiting; returns a ticket for
+        wait_results.  `pcm` ([m][n] float32) is kept alive until collected
+        (pinned memory, e.g. torch .pin_memory().numpy(), overlaps the copy)."""
+        pcm = np.ascontiguousarray(pcm, np.float32)
+        if pcm.ndim != 2 or pcm.shape[0] != self.m:
+            raise ValidationError("sample block channel count does not match the engine")
+        t = C.c_uint64()
+        _capi.check(self.L.sslg_push_samples_async(self.h, f32p(pcm), pcm.shape[1], C.byref(t)))
+        self._inflight = getattr(self, "_inflight", [])
+        self._inflight.append((t.value, pcm))
+        return t.value
+
+    def wait_results(self, ticket: int, cap: int = 4096, want_power: bool = False):
+        """Blocks of every asynchronous push up to `ticket`, in order."""
+        ns = self.music.num_sources
+        blocks = (_capi.BlockOut * max(cap, 1))()
+        idx = np.zeros((cap, ns), np.uint32)
+        pw = np.zeros((cap, ns))
+        low = np.zeros((cap, ns), np.uint8)
+        power = np.zeros((cap, self.dirs)) if want_power else None
+        em = C.c_uint32()
+        try:
+            _capi.check(self.L.sslg_wait_results(self.h, ticket, cap, blocks, u32p(idx), f64p(pw), u8p(low),
+                                                 f64p(power), C.byref(em)))
+        finally:
+            self._inflight = [(t, a) for t, a in getattr(self, "_inflight", []) if t > ticket]
+        n = em.value
+        return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
+                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
+                    low=low[:n].astype(bool), power=None if power is None else power[:n])
+
     def push_device(self, x_dev_ptr: int, nframes: int) -> int:
         em = C.c_uint32()
         _capi.check(self.L.sslg_push_frames_device(self.h, C.c_void_p(x_dev_ptr), nframes, C.byref(em)))
@@ -411,6 +443,7 @@ class Engine:
 
     def reset_window(self):
         _capi.check(self.L.sslg_reset_window(self.h))
+        self._inflight = []
 
     def synchronize(self):
         _capi.check(self.L.sslg_synchronize(self.h))

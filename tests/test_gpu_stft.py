@@ -146,3 +146,44 @@ def test_non_finite_samples_rejected_window_unchanged():
     assert first["n"] <= want["n"]
     eng.close()
     ref.close()
+
+
+def test_async_pushes_match_the_synchronous_stream():
+    """sslg_push_samples_async / sslg_wait_results: many
+    pushes in flight, collected later, give exactly the synchronous results;
+    a non-finite value stops the stream on the device and reports the
+    reference's error; a reset restarts it."""
+    from paper_2504_03373_b200.errors import ValidationError
+
+    g = np.load(GOLDEN)
+    stft = _cfg(g, "hann_band")
+    audio = g["hann_band_audio"]
+    frames = g["hann_band_frames"]
+    ref = _engine(audio.shape[0], stft)
+    want = ref.push(frames, want_power=True)
+    ref.close()
+    eng = _engine(audio.shape[0], stft)
+    tickets = [eng.push_samples_async(audio[:, a:a + 700]) for a in range(0, audio.shape[1], 700)]
+    got = eng.wait_results(tickets[-1], want_power=True)
+    assert got["n"] == want["n"]
+    assert np.array_equal(got["frame_index"], want["frame_index"])
+    assert np.array_equal(got["power"], want["power"])
+    for b in range(got["n"]):
+        c = int(got["count"][b])
+        assert np.array_equal(got["idx"][b][:c], want["idx"][b][:c])
+    # poison: NaN in the second half
+    eng.reset_window()
+    bad = audio.copy()
+    bad[2, 2500] = np.inf
+    t1 = eng.push_samples_async(bad[:, :2000])
+    t2 = eng.push_samples_async(bad[:, 2000:])
+    ok = eng.wait_results(t1)
+    assert ok["n"] > 0
+    with pytest.raises(ValidationError, match="non-finite"):
+        eng.wait_results(t2)
+    with pytest.raises(ValidationError):
+        eng.push_samples(audio[:, :1000])
+    eng.reset_window()
+    again = eng.push_samples(audio, want_power=True)
+    assert np.array_equal(again["power"], want["power"])
+    eng.close()
