@@ -183,7 +183,7 @@ def reference_time_blocks(w, nblocks, threads):
     st = out["stage_s"]
     # stage clocks of the emitting frames: push + normalize + gsvd + spectrum
     # + peaks per block (the T-1 window-filling pushes are not charged)
-    return float(np.sum(st)) / nblocks, st
+    return float(np.sum(st)) / nblocks, st, out
 
 
 def run_reference_arm(args, w, rank, world):
@@ -195,7 +195,7 @@ def run_reference_arm(args, w, rank, world):
         reference_time_blocks(w, per_step, cores)
     times = []
     for _ in range(args.steps):
-        spb, _ = reference_time_blocks(w, per_step, cores)
+        spb, _, _ = reference_time_blocks(w, per_step, cores)
         times.append(spb * per_step)
     total = sum(times)
     value = args.steps * per_step / total
@@ -440,8 +440,19 @@ def main():
             "peaks": {"ms_per_launch": stage[4] / args.steps},
         }
         cpu = None
+        parity = None
         if not args.no_cpu_baseline and world == 1:
             cpu = cpu_baseline(w, args.cpu_sample_blocks)
+            if cpu is not None:
+                ref_out = cpu.pop("_ref_out")
+                def fresh_engine():
+                    e = ssl.Engine(w.m, w.bins, window_frames=w.t, music=ssl.MusicConfig(num_sources=w.ns),
+                                   max_batch=args.batch, device=device)
+                    e.set_noise_model(w.k)
+                    e.set_steering(w.h, w.dirs)
+                    return e
+
+                parity = parity_in_run(w, fresh_engine, ref_out, args.cpu_sample_blocks)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -460,6 +471,7 @@ def main():
             "roofline": roofline,
             "kernels": kernels,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "sslg_push_samples_async + sslg_wait_results (run_locate streaming on pinned host "
                            "PCM: H2D, device STFT, hot path, estimates D2H; one push in flight while the previous "
@@ -653,7 +665,7 @@ def cpu_baseline(w, nblocks):
     except Exception:
         return None
     cores = os.cpu_count() or 1
-    spb, st = reference_time_blocks(w, nblocks, cores)
+    spb, st, ref_out = reference_time_blocks(w, nblocks, cores)
     # the paper's methodology: gsvd() with one thread ("naive" path), 2 blocks
     R = oracle.ref()
     r = R.correlation(w.x[:w.t + 1], w.t)
@@ -666,7 +678,32 @@ def cpu_baseline(w, nblocks):
             "sample": f"{nblocks} consecutive blocks of the same C3 stream through the reference run_locate loop "
                       f"(oracle/_ref = unmodified sslkit, ssl::gsvd batched float path, {cores} threads)",
             "stage_s": {"correlation": st[0], "factorization": st[1], "spectrum": st[2], "peaks": st[3]},
-            "gsvd_us_per_block": 1e6 * st[1] / nblocks}
+            "gsvd_us_per_block": 1e6 * st[1] / nblocks, "_ref_out": ref_out}
+
+
+def parity_in_run(w, eng_factory, ref_out, nblocks, n_fp64=3):
+    """The bench scene's estimates against the reference on the same frames
+    (SURVEY §8(d) parity gates): ranked direction sets vs the reference's
+    production float path on every sampled block, and vs its FP64 oracle path
+    (plus the broadband spectrum's relative error) on the first n_fp64."""
+    import oracle
+
+    eng = eng_factory()
+    frames = w.x[:w.t - 1 + nblocks]
+    out = eng.push(frames, want_power=True)
+    eng.close()
+    same_f = [np.array_equal(out["idx"][b][:out["count"][b]], ref_out["idx"][b][:ref_out["count"][b]])
+              for b in range(nblocks)]
+    R = oracle.ref()
+    mc = oracle.MusicCfg.make(num_sources=w.ns)
+    dbl = R.locate_frames(oracle.Workload(frames[:w.t - 1 + n_fp64], w.k, w.h, w.dirs), w.t, mc, path=2,
+                          threads=os.cpu_count() or 1)
+    same_d = [np.array_equal(out["idx"][b][:out["count"][b]], dbl["idx"][b][:dbl["count"][b]]) for b in range(n_fp64)]
+    rel = max(float(np.max(np.abs(out["power"][b] - dbl["power"][b]) / np.abs(dbl["power"][b])))
+              for b in range(n_fp64))
+    return {"blocks_vs_reference_float_path": nblocks, "same_ranked_directions_float": float(np.mean(same_f)),
+            "blocks_vs_reference_fp64_path": n_fp64, "same_ranked_directions_fp64": float(np.mean(same_d)),
+            "pbar_max_rel_err_vs_fp64": rel}
 
 
 if __name__ == "__main__":
