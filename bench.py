@@ -44,6 +44,12 @@ WORKLOADS = {"c1": "C1 (BASELINE configs[0])", "c2": "C2 (BASELINE configs[1])",
              "c4": "C4 (BASELINE configs[3], 72 az x 19 el grid)"}
 
 
+def scene_label(args, w):
+    return (f"{WORKLOADS[args.config]}: {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, {w.bins} bins, "
+            f"{w.h.shape[0]} directions, {w.ns} targets (0 dB) + 4 rotor sources (-10 dB) + diffuse (-20 dB), "
+            f"K captured from a noise-only recording, T={w.t}, Ns={w.ns}")
+
+
 def frames_from_pcm(w):
     """The scene's STFT frames for the CPU arms (oracle restatement of
     stft_stream, bit-identical to the reference and to the device STFT)."""
@@ -204,8 +210,9 @@ def run_reference_arm(args, w, rank, world):
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": f"{w.name}: {w.m}-ch, {w.bins} bins, {w.h.shape[0]} dirs, T={w.t}, Ns={w.ns}",
-                   "blocks_per_step": per_step, "path": "ssl::gsvd batched float + calc_average_power<float>"},
+        "config": {"workload": scene_label(args, w),
+                   "blocks_per_step": per_step, "path": "ssl::gsvd batched float + calc_average_power<float>",
+                   "input": "STFT frames of the same PCM (the reference's own STFT is not timed)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{per_step} blocks per step of the same C3 stream through the reference "
                                    f"run_locate loop (oracle/_ref, {cores} threads)"},
@@ -457,10 +464,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{WORKLOADS[args.config]}: {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, "
-                                   f"{w.bins} bins, {w.h.shape[0]} directions, {w.ns} targets (0 dB) + 4 rotor "
-                                   f"sources (-10 dB) + diffuse (-20 dB), K captured from a noise-only recording, "
-                                   f"T={w.t}, Ns={w.ns}; PCM input, device STFT",
+            "config": {"workload": scene_label(args, w),
+                       "input": "PCM; value: frames from the device STFT resident in HBM; e2e: PCM from pinned host",
                        "blocks_per_step_per_gpu": args.batch, "arrays": world,
                        "l2": "flushed (256 MiB write) between timed steps" if not args.no_flush else "not flushed",
                        "parallelism": f"array-sharded x{world} (no data-path collective)"},
