@@ -38,12 +38,23 @@ namespace sslg {
 #endif
 constexpr int kLPP = SSLG_JAC_LPP;   // lanes per column pair
 constexpr int kJacThreads = 32 * kLPP;  // 32 column-pair groups
+// small arrays (m <= 16: at most 8 pairs) run 64-thread CTAs with a scratch
+// sized for them, so several bins share an SM instead of one CTA idling 3/4
+template <int MC>
+constexpr int jac_threads() { return (MC > 0 && MC <= 16) ? 64 : kJacThreads; }
 constexpr int kRows = kMaxM / kLPP;  // rows per lane (8)
 constexpr double kReorth = 1e-5;  // re-orthonormalization line (relative to sigma_max)
 constexpr int kZMax = 24;            // largest group handled by the fused picker
 constexpr int kYld = kZMax + 1;      // padded row stride of the coordinate buffer
 // scratch after W: picker coordinates, C^H D products and the packed D^H D
 constexpr int kScratch = kMaxM * (kMaxM + 1) / 2 > kMaxM * kYld ? kMaxM * (kMaxM + 1) / 2 : kMaxM * kYld;
+// scratch entries for a compile-time channel count (0: any m <= 64): the
+// packed Cholesky (m(m+1)/2), the sequential picker's rows (m kYld) and the
+// concurrent pickers' G and Z slices (<= 2 m^2 for m <= 16)
+constexpr int cmax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+__host__ __device__ constexpr int scratch_entries(int mc) {
+    return (mc > 0 && mc <= 16) ? cmax3(mc * (mc + 1) / 2, mc * kYld, 2 * mc * mc) : kScratch;
+}
 
 struct CanonScratch {
     double nrm[kMaxM];
@@ -529,7 +540,7 @@ __device__ __forceinline__ double fast_sqrt(double x) { return x > 0 ? x * fast_
 // the serial part of every step.
 template <int MC>
 __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
-    constexpr int QL = kJacThreads / kMaxM;  // lanes per column (4 at 256 threads, 8 at 512)
+    constexpr int QL = jac_threads<MC>() / kMaxM > 0 ? jac_threads<MC>() / kMaxM : 1;  // lanes per column
     constexpr int RP = MC > 0 ? (MC + QL - 1) / QL : kMaxM / QL;
     const int t = threadIdx.x, c = t / QL, l = t % QL, lane = t & 31;
     const bool own = c < m;
@@ -864,7 +875,7 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
 // MC > 0: channel count fixed at compile time (loop bounds, predicates and
 // addressing fold away); MC == 0: any m <= 64 at run time.
 template <int MC>
-__global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
+__global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2) jacobi_kernel(GsvdArgs a) {
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = MC > 0 ? MC : a.m;
@@ -1141,10 +1152,10 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
             s_off[ngt] = off;
         }
         __syncthreads();
-        const bool concurrent = s_off[ngt] <= kScratch;
+        const bool concurrent = s_off[ngt] <= scratch_entries(MC);
         {
             const int warp = tid / kWarp;
-            for (int gi = warp; gi < ngt; gi += kJacThreads / kWarp) {
+            for (int gi = warp; gi < ngt; gi += jac_threads<MC>() / kWarp) {
                 int i0, d;
                 grp(gi, i0, d);
                 bool ok = false;
@@ -1173,7 +1184,7 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
         }
         // phase rule (gsvd.cpp:545-564): warp per vector
         const int warp = tid / kWarp, lane = tid % kWarp;
-        for (int rk = warp; rk < m; rk += kJacThreads / kWarp) {
+        for (int rk = warp; rk < m; rk += jac_threads<MC>() / kWarp) {
             const int j = s_perm[rk];
             double best = -1;
             int bi = 0;
@@ -1227,20 +1238,18 @@ __global__ void __launch_bounds__(kJacThreads, 2) jacobi_kernel(GsvdArgs a) {
     }
 }
 
-size_t jacobi_smem_bytes(int m) { return (size_t)m * m * sizeof(double2) + (size_t)kScratch * sizeof(double2); }
-
 void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
-    const size_t smem = jacobi_smem_bytes(a.m);
-    auto launch = [&](auto kern) {
+    auto launch = [&](auto kern, int threads, int mc) {
+        const size_t smem = (size_t)a.m * a.m * sizeof(double2) + (size_t)scratch_entries(mc) * sizeof(double2);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<nblk * a.bins, kJacThreads, smem, s>>>(a);
+        kern<<<nblk * a.bins, threads, smem, s>>>(a);
     };
     switch (a.m) {  // the BASELINE configs' channel counts get specialized code
-        case 8: launch(jacobi_kernel<8>); break;
-        case 16: launch(jacobi_kernel<16>); break;
-        case 60: launch(jacobi_kernel<60>); break;
-        case 64: launch(jacobi_kernel<64>); break;
-        default: launch(jacobi_kernel<0>); break;
+        case 8: launch(jacobi_kernel<8>, jac_threads<8>(), 8); break;
+        case 16: launch(jacobi_kernel<16>, jac_threads<16>(), 16); break;
+        case 60: launch(jacobi_kernel<60>, jac_threads<60>(), 60); break;
+        case 64: launch(jacobi_kernel<64>, jac_threads<64>(), 64); break;
+        default: launch(jacobi_kernel<0>, jac_threads<0>(), 0); break;
     }
 }
 
