@@ -91,13 +91,16 @@ __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
 // conflict-free.  The 16 threads holding the same directions and different
 // vector slices are adjacent lanes; their partial denominators meet in a
 // 4-level shuffle tree, identical for every direction (exact ties survive).
-constexpr int kTileD = 4, kTileN = 4, kSlices = 16, kDirTiles = 16;
-constexpr int kChunk2 = kTileD * kDirTiles;  // 64 directions per CTA
+constexpr int kTileD = 4, kTileN = 4, kSlices = 16;
 constexpr int kNPad = kTileN * kSlices;      // 64 vector slots
 constexpr int kEStride = kNPad + 1;          // double2 row stride of the staged noise vectors (bank spread)
-constexpr int kHStride = kChunk2 + 2;        // float2 row stride of the staged steering (16-B aligned rows)
 
-__global__ void __launch_bounds__(256, 2) spectrum_tiled_kernel(SpecArgs a, int nblk, int nchunk) {
+// DT direction tiles of 4 per CTA (16 lanes each): 64 directions at DT = 16
+// (large grids), the whole 72-direction ring at DT = 18.
+template <int DT>
+__global__ void __launch_bounds__(16 * DT, 2) spectrum_tiled_kernel(SpecArgs a, int nblk, int nchunk) {
+    constexpr int kChunk2 = kTileD * DT;
+    constexpr int kHStride = kChunk2 + 2;  // float2 row stride of the staged steering (16-B aligned rows)
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = a.m;
@@ -280,12 +283,22 @@ void spectrum_shape(int m, int ns, int dirs, int& dchunk, int& nsplit, size_t& s
 }
 
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
-    if (a.dirs >= 256 && a.m - a.ns <= kNPad) {  // large grids: register-tiled kernel
-        const size_t smem2 = (size_t)a.m * kEStride * sizeof(double2) + (size_t)a.m * kHStride * sizeof(float2);
-        cudaFuncSetAttribute(spectrum_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        const int nchunk = (a.dirs + kChunk2 - 1) / kChunk2;
-        spectrum_tiled_kernel<<<nblk * a.bins * nchunk, 256, smem2, s>>>(a, nblk, nchunk);
-        return;
+    auto tiled = [&](auto kern, int dt) {
+        const int chunk = kTileD * dt;
+        const size_t smem2 = (size_t)a.m * kEStride * sizeof(double2) + (size_t)a.m * (chunk + 2) * sizeof(float2);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        const int nchunk = (a.dirs + chunk - 1) / chunk;
+        kern<<<nblk * a.bins * nchunk, 16 * dt, smem2, s>>>(a, nblk, nchunk);
+    };
+    if (a.m - a.ns <= kNPad) {  // register-tiled kernel
+        if (a.dirs >= 256) {
+            tiled(spectrum_tiled_kernel<16>, 16);
+            return;
+        }
+        if (a.dirs > 64 && a.dirs <= 72) {
+            tiled(spectrum_tiled_kernel<18>, 18);
+            return;
+        }
     }
     size_t smem;
     spectrum_shape(a.m, a.ns, a.dirs, a.dchunk, a.nsplit, smem);
