@@ -74,10 +74,10 @@ struct CanonScratch {
 
 // Completes the basis: the columns below the drop line (list D, rank order)
 // are orthonormalized against the certified columns C and then among
-// themselves.  Block form: two passes of D -= C (C^H D) (Gram product in the
-// scratch G, |C||D| <= m^2/4 entries), then one warp runs two classical
-// Gram-Schmidt passes per column of D against the earlier ones (8 dots per
-// butterfly) and normalizes it.  Clears cs.eligible if a column collapses.
+// themselves.  Block form: D -= C (C^H D) (Gram product in the scratch G,
+// |C||D| <= m^2/4 entries), repeated only where the first pass removed more
+// than half of a column's energy, then CholeskyQR2 of D (the rank-order
+// Gram-Schmidt result).  Clears cs.eligible if a column collapses.
 template <int MC>
 __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& cs) {
     const int m = MC > 0 ? MC : m_rt;
