@@ -69,7 +69,7 @@ struct CanonScratch {
     int certcols[kMaxM];      // certified columns
     double invd[kMaxM];       // 1 / L_jj of the CholeskyQR (column norms before it)
     double dn2[kMaxM];        // column norms after the first projection
-    int ngroups, nvanish, eligible, ndropped, ncert, collapsed;
+    int ngroups, nvanish, eligible, ndropped, ncert, collapsed, again;
 };
 
 // Completes the basis: the columns below the drop line (list D, rank order)
@@ -209,6 +209,18 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& c
                 if (t == 0) invd[j] = inv;
                 __syncwarp();
             }
+            if (t == 0 && !cs.collapsed) {
+                // CholeskyQR loses orthogonality like eps kappa(D)^2; with the
+                // Cholesky diagonal spread (a lower bound on kappa) below 100 the
+                // first pass is already orthonormal to ~1e-12 and the second is
+                // skipped
+                double lo = invd[0], hi = invd[0];
+                for (int j = 1; j < nd; ++j) {
+                    lo = fmin(lo, invd[j]);
+                    hi = fmax(hi, invd[j]);
+                }
+                cs.again = hi <= 100.0 * lo ? 0 : 1;
+            }
         }
         __syncthreads();
         if (cs.collapsed) return;  // uniform: written before the barrier above
@@ -238,6 +250,7 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& c
             }
         }
         __syncthreads();
+        if (pass == 0 && !cs.again) break;  // uniform: written before the barrier above
     }
 }
 
