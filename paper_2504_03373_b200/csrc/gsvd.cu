@@ -44,7 +44,7 @@ template <int MC>
 constexpr int jac_threads() { return (MC > 0 && MC <= 16) ? 64 : kJacThreads; }
 constexpr int kRows = kMaxM / kLPP;  // rows per lane (8)
 constexpr double kReorth = 1e-5;  // re-orthonormalization line (relative to sigma_max)
-constexpr int kZMax = 24;            // largest group handled by the fused picker
+constexpr int kZMax = 28;            // largest group handled by the fused picker
 constexpr int kYld = kZMax + 1;      // padded row stride of the coordinate buffer
 // scratch after W: picker coordinates, C^H D products and the packed D^H D
 constexpr int kScratch = kMaxM * (kMaxM + 1) / 2 > kMaxM * kYld ? kMaxM * (kMaxM + 1) / 2 : kMaxM * kYld;
@@ -328,19 +328,27 @@ __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_
     return s_ok != 0;
 }
 
-// Warp-private form of pick_fast for the concurrent canonicalization: one
-// warp per group (vanishing block or tied group), group columns s_perm[i0+k],
-// scratch G [d][d] and result Z [d][d] (coordinate k of vector t at k*d+t)
-// private to the warp; no block barrier.  Returns whether the first d
-// candidates are all accepted (else nothing usable is written).
+// Concurrent form of pick_fast for the fused canonicalization, in three
+// stages over all groups at once (group columns s_perm[i0+k], scratch slice
+// G [d][d] then Z [d][d], coordinate k of vector t at k*d+t):
+//   gram_group   G = Y^H Y, y_j[k] = conj(W[cols[k]][j]), by the whole CTA;
+//   chol_group   one warp per group: the Cholesky G = R^H R with the
+//                acceptance test R_jj > 0.05 n0_j of pick_orthonormal
+//                (gsvd.cpp:404-436) at every step; false when a candidate
+//                would be rejected (the caller then runs the sequential picker);
+//   z_rows       Z = Y R^-1, kZL threads per coordinate row, by the whole CTA.
 template <int MC>
-__device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, double2* Z, double* n0b, double* ivb,
-                               int m_rt, int d, bool unit_norm0) {
+__device__ __forceinline__ void gram_group(const double2* W, const int* cols, double2* G, int m_rt, int d) {
     const int m = MC > 0 ? MC : m_rt;
-    const int lane = threadIdx.x & 31;
-    for (int e = lane; e < d * d; e += kWarp) {
-        const int a = e / d, b = e % d;
-        if (b < a) continue;
+    constexpr int nt = jac_threads<MC>();
+    const int np = d * (d + 1) / 2;
+    for (int e = threadIdx.x; e < np; e += nt) {
+        // e -> (a, b), a <= b, row-major over the upper triangle
+        int a = (int)((2.0f * d + 1.0f - sqrtf((2.0f * d + 1.0f) * (2.0f * d + 1.0f) - 8.0f * e)) * 0.5f);
+        if (a < 0) a = 0;
+        while (a > 0 && a * d - a * (a - 1) / 2 > e) --a;
+        while ((a + 1) * d - (a + 1) * a / 2 <= e) ++a;
+        const int b = a + (e - (a * d - a * (a - 1) / 2));
         double gx = 0, gy = 0;
         for (int k = 0; k < d; ++k) {
             const double2 wa = W[cols[k] * m + a], wb = W[cols[k] * m + b];
@@ -349,7 +357,10 @@ __device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, do
         }
         G[a * d + b] = make_double2(gx, gy);
     }
-    __syncwarp();
+}
+
+__device__ __forceinline__ bool chol_group(double2* G, double* n0b, double* ivb, int d, bool unit_norm0) {
+    const int lane = threadIdx.x & 31;
     if (lane < d) n0b[lane] = unit_norm0 ? 1.0 : sqrt(G[lane * d + lane].x);
     __syncwarp();
     for (int j = 0; j < d; ++j) {
@@ -360,14 +371,15 @@ __device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, do
         const double inv = 1.0 / rjj;
         for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
         __syncwarp();
-        const int n = d - j - 1;
-        for (int e = lane; e < n * n; e += kWarp) {
-            const int a = j + 1 + e / n, b = j + 1 + e % n;
-            if (b < a) continue;
-            const double2 ra = G[j * d + a], rb = G[j * d + b];
-            double2& g = G[a * d + b];
-            g.x -= fma(ra.x, rb.x, ra.y * rb.y);
-            g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+        // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b]
+        for (int b = j + 1 + lane; b < d; b += kWarp) {
+            const double2 rb = G[j * d + b];
+            for (int a = j + 1; a <= b; ++a) {
+                const double2 ra = G[j * d + a];
+                double2& g = G[a * d + b];
+                g.x -= fma(ra.x, rb.x, ra.y * rb.y);
+                g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+            }
         }
         if (lane == 0) {
             G[j * d + j] = make_double2(rjj, 0.0);
@@ -375,39 +387,58 @@ __device__ bool pick_fast_warp(const double2* W, const int* cols, double2* G, do
         }
         __syncwarp();
     }
-    if (lane < d) {  // Z = Y R^-1, lane = coordinate
-        const int k = lane;
-        for (int tt = 0; tt < d; ++tt) {
-            const double2 w = W[cols[k] * m + tt];
-            double2 acc = make_double2(w.x, -w.y);
-            for (int s2 = 0; s2 < tt; ++s2) acc = csub(acc, cmul(Z[k * d + s2], G[s2 * d + tt]));
-            Z[k * d + tt] = cscale(ivb[tt], acc);
-        }
-    }
-    __syncwarp();
     return true;
 }
 
-// New columns of one group from a warp-private Z: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
+// Z[k][tt] = (y_tt[k] - sum_{s<tt} Z[k][s] R[s][tt]) / R[tt][tt] for row k of
+// one group; the kZL lanes split the sum (lane part keeps, and alone reads
+// back, the entries s = part mod kZL).
+template <int kZL>
+__device__ __forceinline__ void z_row(const double2* W, const int* cols, const double2* G, double2* Z,
+                                      const double* ivb, int m, int d, int k, int part) {
+    for (int tt = 0; tt < d; ++tt) {
+        double2 acc = make_double2(0, 0);
+        for (int s2 = part; s2 < tt; s2 += kZL) {
+            const double2 zv = Z[k * d + s2], r = G[s2 * d + tt];
+            acc.x = fma(zv.x, r.x, fma(-zv.y, r.y, acc.x));
+            acc.y = fma(zv.x, r.y, fma(zv.y, r.x, acc.y));
+        }
+        acc = group_sum2<kZL>(acc);
+        if (part == tt % kZL) {
+            const double2 w = W[cols[k] * m + tt];
+            Z[k * d + tt] = cscale(ivb[tt], make_double2(w.x - acc.x, -w.y - acc.y));
+        }
+    }
+}
+
+// New columns of one group from a Z slice: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
 template <int MC>
 __device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const double2* Z) {
     const int m = MC > 0 ? MC : m_rt;
+    constexpr int nt = jac_threads<MC>();
+    constexpr int kOut = ((MC > 0 ? MC : kMaxM) * kZMax + nt - 1) / nt;
     const int t = threadIdx.x;
-    double2 out[6];
-    int cnt = 0;
-    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) {
-        const int i = e % m, sv = e / m;
-        double2 acc = make_double2(0, 0);
-        for (int k = 0; k < d; ++k) {
-            const double2 a = W[cols[k] * m + i], b = Z[k * d + sv];
-            acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-            acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+    double2 out[kOut];
+#pragma unroll
+    for (int c = 0; c < kOut; ++c) {
+        const int e = t + c * nt;
+        if (e < m * d) {
+            const int i = e % m, sv = e / m;
+            double2 acc = make_double2(0, 0);
+            for (int k = 0; k < d; ++k) {
+                const double2 a = W[cols[k] * m + i], b = Z[k * d + sv];
+                acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+                acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+            }
+            out[c] = acc;
         }
-        out[cnt] = acc;
     }
     __syncthreads();
-    cnt = 0;
-    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) W[cols[e / m] * m + (e % m)] = out[cnt];
+#pragma unroll
+    for (int c = 0; c < kOut; ++c) {
+        const int e = t + c * nt;
+        if (e < m * d) W[cols[e / m] * m + (e % m)] = out[c];
+    }
     __syncthreads();
 }
 
@@ -1136,11 +1167,8 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
     const bool fused = cs.eligible;
     if (a.canonical && fused) {
         const int z = cs.nvanish;
-        // all groups (the vanishing block first, then the tied groups) are
-        // disjoint column sets: one warp each runs the QR-form picker at
-        // once, each in its own slice of the scratch (G then Z, 2 d^2
-        // entries); groups the fast path rejects, or that do not fit, take
-        // the sequential picker afterwards
+        // the groups (the vanishing block first, then the tied groups) are
+        // disjoint column sets; each runs the QR-form picker
         const int ngt = cs.ngroups + (z > 0 ? 1 : 0);
         auto grp = [&](int gi, int& i0, int& d) {
             if (z > 0 && gi == 0) {
@@ -1154,36 +1182,59 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
         };
         __shared__ int s_fast[kMaxM];
         __shared__ int s_off[kMaxM + 1];
+        __shared__ int s_row[kMaxM + 1];
         if (tid == 0) {
-            int off = 0;
+            int off = 0, rows = 0;
             for (int gi = 0; gi < ngt; ++gi) {
                 int i0, d;
                 grp(gi, i0, d);
                 s_off[gi] = off;
+                s_row[gi] = rows;
                 off += 2 * d * d;
+                rows += d;
             }
             s_off[ngt] = off;
+            s_row[ngt] = rows;
         }
         __syncthreads();
+        // groups that do not fit the scratch together, or exceed kZMax, take
+        // the sequential picker afterwards
         const bool concurrent = s_off[ngt] <= scratch_entries(MC);
-        {
+        if (concurrent) {
+            for (int gi = 0; gi < ngt; ++gi) {
+                int i0, d;
+                grp(gi, i0, d);
+                if (d <= kZMax) gram_group<MC>(W, s_perm + i0, Y + s_off[gi], m, d);
+            }
+            __syncthreads();
             const int warp = tid / kWarp;
             for (int gi = warp; gi < ngt; gi += jac_threads<MC>() / kWarp) {
                 int i0, d;
                 grp(gi, i0, d);
-                bool ok = false;
-                if (concurrent && d <= kZMax) {
-                    double2* G = Y + s_off[gi];
-                    ok = pick_fast_warp<MC>(W, s_perm + i0, G, G + d * d, cs.norm0 + i0, cs.nrm + i0, m, d, z > 0 && gi == 0);
-                }
+                const bool ok =
+                    d <= kZMax && chol_group(Y + s_off[gi], cs.norm0 + i0, cs.nrm + i0, d, z > 0 && gi == 0);
                 if ((tid & 31) == 0) s_fast[gi] = ok ? 1 : 0;
             }
-        }
-        __syncthreads();
-        for (int gi = 0; gi < ngt; ++gi) {
-            int i0, d;
-            grp(gi, i0, d);
-            if (s_fast[gi]) apply_span_z<MC>(W, m, d, s_perm + i0, Y + s_off[gi] + d * d);
+            __syncthreads();
+            constexpr int kZL = 4;
+            for (int r = tid / kZL; r < s_row[ngt]; r += jac_threads<MC>() / kZL) {
+                int gi = 0;
+                while (s_row[gi + 1] <= r) ++gi;
+                if (!s_fast[gi]) continue;  // uniform over the kZL lanes of the row
+                int i0, d;
+                grp(gi, i0, d);
+                const double2* G = Y + s_off[gi];
+                z_row<kZL>(W, s_perm + i0, G, Y + s_off[gi] + d * d, cs.nrm + i0, m, d, r - s_row[gi], tid % kZL);
+            }
+            __syncthreads();
+            for (int gi = 0; gi < ngt; ++gi) {
+                int i0, d;
+                grp(gi, i0, d);
+                if (s_fast[gi]) apply_span_z<MC>(W, m, d, s_perm + i0, Y + s_off[gi] + d * d);
+            }
+        } else {
+            for (int gi = tid; gi < ngt; gi += jac_threads<MC>()) s_fast[gi] = 0;
+            __syncthreads();
         }
         mark(7);
         for (int gi = 0; gi < ngt; ++gi) {  // after every Z slice is consumed: the scratch is free
