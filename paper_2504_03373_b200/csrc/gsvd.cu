@@ -328,6 +328,16 @@ __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_
     return s_ok != 0;
 }
 
+// Upper-triangle packed index of (a, b), a <= b, of a d x d matrix.
+__device__ __forceinline__ int tri(int a, int b, int d) { return a * d - a * (a - 1) / 2 + (b - a); }
+__device__ __forceinline__ void tri_ab(int e, int d, int& a, int& b) {
+    a = (int)((2.0f * d + 1.0f - sqrtf((2.0f * d + 1.0f) * (2.0f * d + 1.0f) - 8.0f * e)) * 0.5f);
+    if (a < 0) a = 0;
+    while (a > 0 && a * d - a * (a - 1) / 2 > e) --a;
+    while ((a + 1) * d - (a + 1) * a / 2 <= e) ++a;
+    b = a + (e - (a * d - a * (a - 1) / 2));
+}
+
 // Concurrent form of pick_fast for the fused canonicalization, in three
 // stages over all groups at once (group columns s_perm[i0+k], scratch slice
 // G [d][d] then Z [d][d], coordinate k of vector t at k*d+t):
@@ -343,12 +353,8 @@ __device__ __forceinline__ void gram_group(const double2* W, const int* cols, do
     constexpr int nt = jac_threads<MC>();
     const int np = d * (d + 1) / 2;
     for (int e = threadIdx.x; e < np; e += nt) {
-        // e -> (a, b), a <= b, row-major over the upper triangle
-        int a = (int)((2.0f * d + 1.0f - sqrtf((2.0f * d + 1.0f) * (2.0f * d + 1.0f) - 8.0f * e)) * 0.5f);
-        if (a < 0) a = 0;
-        while (a > 0 && a * d - a * (a - 1) / 2 > e) --a;
-        while ((a + 1) * d - (a + 1) * a / 2 <= e) ++a;
-        const int b = a + (e - (a * d - a * (a - 1) / 2));
+        int a, b;
+        tri_ab(e, d, a, b);  // row-major over the upper triangle
         double gx = 0, gy = 0;
         for (int k = 0; k < d; ++k) {
             const double2 wa = W[cols[k] * m + a], wb = W[cols[k] * m + b];
@@ -409,6 +415,169 @@ __device__ __forceinline__ void z_row(const double2* W, const int* cols, const d
             Z[k * d + tt] = cscale(ivb[tt], make_double2(w.x - acc.x, -w.y - acc.y));
         }
     }
+}
+
+// The vanishing block when it exceeds kZMax (short windows, T < m / 2): its
+// projector is written through the lead vectors B (ranks 0..m-z-1),
+// P = I - B B^H — the form the reference itself builds (gsvd.cpp:466-503) —
+// so no z x z buffer is needed.  G = P[0:z, 0:z] (the candidates e_0..e_z-1)
+// goes packed into the scratch, its Cholesky runs with the acceptance test
+// (candidate norms 1), and row i of the new block, P[i, 0:z] R^-1, is formed
+// and back-substituted in place in row i of the vanishing columns.  False
+// (nothing written) when a candidate would be rejected: seq_vanish then
+// runs the reference's sequential picker.
+template <int MC>
+__device__ bool big_vanish(double2* W, const int* perm, int m_rt, int z, double2* Rp, double* ivb) {
+    const int m = MC > 0 ? MC : m_rt;
+    constexpr int nt = jac_threads<MC>();
+    constexpr int kZL = 4;
+    const int tid = threadIdx.x;
+    const int lead = m - z;
+    const int* vcols = perm + lead;
+    __shared__ int s_ok;
+    for (int e = tid; e < z * (z + 1) / 2; e += nt) {
+        int a, b;
+        tri_ab(e, z, a, b);
+        double gx = 0, gy = 0;
+        for (int l = 0; l < lead; ++l) {
+            const double2 wa = W[perm[l] * m + a], wb = W[perm[l] * m + b];
+            gx = fma(wa.x, wb.x, fma(wa.y, wb.y, gx));
+            gy = fma(wa.y, wb.x, fma(-wa.x, wb.y, gy));
+        }
+        Rp[e] = make_double2((a == b ? 1.0 : 0.0) - gx, -gy);
+    }
+    __syncthreads();
+    if (tid < kWarp) {
+        const int lane = tid;
+        bool ok = true;
+        for (int j = 0; j < z; ++j) {
+            const double gjj = Rp[tri(j, j, z)].x;
+            const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
+            if (!(rjj > 0.05)) {  // acceptance test, n0 = 1 (gsvd.cpp:404-436)
+                ok = false;
+                break;
+            }
+            const double inv = 1.0 / rjj;
+            const int rj = tri(j, j, z);
+            for (int b = j + 1 + lane; b < z; b += kWarp) Rp[rj + b - j] = cscale(inv, Rp[rj + b - j]);
+            __syncwarp();
+            for (int b = j + 1 + lane; b < z; b += kWarp) {
+                const double2 rb = Rp[rj + b - j];
+                for (int a2 = j + 1; a2 <= b; ++a2) {
+                    const double2 ra = Rp[rj + a2 - j];
+                    double2& g = Rp[tri(a2, b, z)];
+                    g.x -= fma(ra.x, rb.x, ra.y * rb.y);
+                    g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+                }
+            }
+            if (lane == 0) {
+                Rp[rj] = make_double2(rjj, 0.0);
+                ivb[j] = inv;
+            }
+            __syncwarp();
+        }
+        if (lane == 0) s_ok = ok ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_ok) return false;
+    // row i: x_t = P[i][t] into W[vcols[t]][i] (lane part owns t = part mod
+    // kZL), then w R = x by forward substitution, in place
+    const int part = tid % kZL;
+    for (int i = tid / kZL; i < m; i += nt / kZL) {
+        for (int t = part; t < z; t += kZL) {
+            double gx = 0, gy = 0;
+            for (int l = 0; l < lead; ++l) {
+                const double2 wa = W[perm[l] * m + i], wb = W[perm[l] * m + t];
+                gx = fma(wa.x, wb.x, fma(wa.y, wb.y, gx));
+                gy = fma(wa.y, wb.x, fma(-wa.x, wb.y, gy));
+            }
+            W[vcols[t] * m + i] = make_double2((i == t ? 1.0 : 0.0) - gx, -gy);
+        }
+        for (int t = 0; t < z; ++t) {
+            double2 acc = make_double2(0, 0);
+            for (int s2 = part; s2 < t; s2 += kZL) {
+                const double2 wv = W[vcols[s2] * m + i], r = Rp[tri(s2, t, z)];
+                acc.x = fma(wv.x, r.x, fma(-wv.y, r.y, acc.x));
+                acc.y = fma(wv.x, r.y, fma(wv.y, r.x, acc.y));
+            }
+            acc = group_sum2<kZL>(acc);
+            if (part == t % kZL) {
+                const double2 x = W[vcols[t] * m + i];
+                W[vcols[t] * m + i] = cscale(ivb[t], make_double2(x.x - acc.x, x.y - acc.y));
+            }
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
+// The reference's sequential picker (pick_orthonormal, gsvd.cpp:404-436) for
+// a vanishing block big_vanish could not take in one pass (a candidate
+// rejected): candidates e_j in index order over the three threshold passes,
+// each projected twice against the lead vectors B and the vectors already
+// taken; accepted vectors go straight into the vanishing columns (the old
+// basis of the block is not needed in this representation).  Thread i < m
+// holds c[i]; cbuf / dots are m-entry scratch.
+template <int MC>
+__device__ void seq_vanish(double2* W, const int* perm, int m_rt, int z, double2* cbuf, double2* dots) {
+    const int m = MC > 0 ? MC : m_rt;
+    constexpr int nt = jac_threads<MC>();
+    constexpr int nw = nt / kWarp;
+    const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
+    const int lead = m - z;
+    const int* vcols = perm + lead;
+    __shared__ double s_red[nw];
+    auto project = [&](double2& c, const int* cols, int n) {
+        if (n == 0) return;
+        if (tid < m) cbuf[tid] = c;
+        __syncthreads();
+        for (int l = warp; l < n; l += nw) {
+            double2 d = make_double2(0, 0);
+            for (int i = lane; i < m; i += kWarp) {
+                const double2 b = W[cols[l] * m + i], v = cbuf[i];
+                d.x = fma(b.x, v.x, fma(b.y, v.y, d.x));
+                d.y = fma(b.x, v.y, fma(-b.y, v.x, d.y));
+            }
+            d = group_sum2<kWarp>(d);
+            if (lane == 0) dots[l] = d;
+        }
+        __syncthreads();
+        if (tid < m)
+            for (int l = 0; l < n; ++l) {
+                const double2 b = W[cols[l] * m + tid], d = dots[l];
+                c.x -= fma(d.x, b.x, -d.y * b.y);
+                c.y -= fma(d.x, b.y, d.y * b.x);
+            }
+    };
+    unsigned long long used = 0;
+    int taken = 0;
+    const double thresholds[3] = {0.05, 1e-8, 0.0};
+    for (int tp = 0; tp < 3 && taken < z; ++tp) {
+        for (int j = 0; j < m && taken < z; ++j) {
+            if ((used >> j) & 1ull) continue;
+            double2 c = make_double2(tid == j ? 1.0 : 0.0, 0.0);
+            for (int pass = 0; pass < 2; ++pass) {
+                project(c, perm, lead);
+                project(c, vcols, taken);
+            }
+            double v = tid < m ? fma(c.x, c.x, c.y * c.y) : 0.0;
+            v = group_sum<kWarp>(v);
+            if (lane == 0) s_red[warp] = v;
+            __syncthreads();
+            double n2 = 0;
+#pragma unroll
+            for (int w = 0; w < nw; ++w) n2 += s_red[w];
+            const double nrm = sqrt(n2);
+            __syncthreads();  // s_red and cbuf reused by the next candidate
+            if (!(nrm > thresholds[tp]) || !(nrm > 0)) continue;
+            if (tid < m) W[vcols[taken] * m + tid] = cscale(1.0 / nrm, c);
+            used |= 1ull << j;
+            ++taken;
+        }
+    }
+    // unfilled slots stay zero, as the reference's zero-initialized output
+    for (int e = tid; e < (z - taken) * m; e += nt) W[vcols[taken + e / m] * m + e % m] = make_double2(0, 0);
+    __syncthreads();
 }
 
 // New columns of one group from a Z slice: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
@@ -1114,7 +1283,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
         int z = 0;
         while (z < m && s_sig[s_perm[m - 1 - z]] <= gap) ++z;
         const int lead_end = m - z;
-        int ng = 0, dmax = z;
+        int ng = 0, dmax = 0;  // the vanishing block has no size limit (big_vanish)
         for (int i = 0; i < lead_end;) {
             int end = i;
             while (end + 1 < lead_end && s_sig[s_perm[end]] - s_sig[s_perm[end + 1]] <= gap) ++end;
@@ -1164,9 +1333,14 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
     // canonicalizes them (the generic one reads the lead vectors too)
     if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis<MC>(W, Y, m, cs);
     mark(4);
-    const bool fused = cs.eligible;
+    bool fused = cs.eligible;
+    int zf = cs.nvanish;  // the vanishing block, when the group machinery below takes it
+    if (a.canonical && fused && zf > kZMax) {
+        if (!big_vanish<MC>(W, s_perm, m, zf, Y, cs.nrm)) seq_vanish<MC>(W, s_perm, m, zf, Y, Y + kMaxM);
+        zf = 0;
+    }
     if (a.canonical && fused) {
-        const int z = cs.nvanish;
+        const int z = zf;
         // the groups (the vanishing block first, then the tied groups) are
         // disjoint column sets; each runs the QR-form picker
         const int ngt = cs.ngroups + (z > 0 ? 1 : 0);

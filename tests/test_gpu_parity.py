@@ -381,3 +381,59 @@ def test_generic_and_max_channel_counts_against_oracle(port, m):
         assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
         # vectors: compare subspaces of well-separated values and the vectors themselves
         assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, (m, rank)
+
+
+@pytest.mark.parametrize("rank", [1, 8, 24])
+def test_short_window_vanishing_block_against_oracle(port, rank):
+    """Short windows (T < m/2 at m = 60): the vanishing block exceeds the
+    coordinate-space picker's kZMax and is canonicalized through the lead
+    vectors' projector in the fused epilogue (big_vanish); the canonical
+    bases must match the oracle's (canonicalize_subspaces, gsvd.cpp:381-565)."""
+    from paper_2504_03373_b200 import ssl
+
+    m, bins = 60, 4
+    rng = np.random.default_rng(77 + rank)
+    kb = rng.standard_normal((bins, m, m)) + 1j * rng.standard_normal((bins, m, m))
+    k = (kb @ kb.conj().transpose(0, 2, 1) / m + 0.5 * np.eye(m)).astype(np.complex64)
+    xb = rng.standard_normal((bins, m, rank)) + 1j * rng.standard_normal((bins, m, rank))
+    r = (xb @ xb.conj().transpose(0, 2, 1) / rank).astype(np.complex64)
+    eng = ssl.Engine(m, bins, window_frames=2, max_batch=2)
+    eng.set_noise_model(k)
+    sigma, e, _, conv = eng.gsvd(r)
+    eng.close()
+    want = port.gsvd_reference(k, r, threads=4)
+    smax = want["sigma"][:, :1]
+    assert np.all(conv)
+    assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+    assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, rank
+
+
+@pytest.mark.parametrize("rank", [6, 30])
+def test_vanishing_block_with_rejected_candidates(port, rank):
+    """Unit vectors inside the kept span are rejected by the picker's
+    acceptance test (pick_orthonormal, gsvd.cpp:404-436): with e_0 and e_2 in
+    range(R) the first pass skips them — the coordinate-space path (rank 30,
+    z = 30 > kZMax: sequential fallback after big_vanish) and the small-block
+    path (rank 6) must still match the oracle."""
+    from paper_2504_03373_b200 import ssl
+
+    m, bins = 60, 2
+    rng = np.random.default_rng(5 + rank)
+    x = rng.standard_normal((bins, m, rank)) + 1j * rng.standard_normal((bins, m, rank))
+    x[:, 0, 2:] = 0
+    x[:, 2, 2:] = 0
+    x[:, :, 0] = 0
+    x[:, :, 1] = 0
+    x[:, 0, 0] = 3.0
+    x[:, 2, 1] = 2.0
+    r = (x @ x.conj().transpose(0, 2, 1) / rank).astype(np.complex64)
+    k = np.broadcast_to(np.eye(m, dtype=np.complex64), (bins, m, m)).copy()
+    eng = ssl.Engine(m, bins, window_frames=2, max_batch=2)
+    eng.set_noise_model(k)
+    sigma, e, _, conv = eng.gsvd(r)
+    eng.close()
+    want = port.gsvd_reference(k, r, threads=4)
+    smax = want["sigma"][:, :1]
+    assert np.all(conv)
+    assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+    assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, rank

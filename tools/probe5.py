@@ -18,14 +18,15 @@ def scene(kind):
     return w, x
 
 
+T = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 for kind in ("pcm", "frames"):
     w, x = scene(kind)
-    eng = ssl.Engine(60, 257, window_frames=50, music=ssl.MusicConfig(num_sources=2), max_batch=32)
+    eng = ssl.Engine(60, 257, window_frames=T, music=ssl.MusicConfig(num_sources=2), max_batch=32)
     eng.set_noise_model(w.k); eng.set_steering(w.h, w.dirs)
     # sequential frames (a repeated push would duplicate frames in the window
     # and halve R's rank)
-    eng.push(x[:50]); eng.push(x[50:82]); eng.synchronize()
-    eng.push(x[82:114]); ms = eng.stage_ms()
+    eng.push(x[:T]); eng.push(x[T:T + 32]); eng.synchronize()
+    eng.push(x[T + 32:T + 64]); ms = eng.stage_ms()
     res = eng.read_results(32, sigma=True)
     sg = res["sigma"].reshape(-1, 60)
     conv = res["conv"].reshape(-1)
