@@ -28,6 +28,7 @@ __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_dou
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 __device__ __forceinline__ double2 f2d(float2 a) { return make_double2((double)a.x, (double)a.y); }
+__device__ __forceinline__ double2 f2d(double2 a) { return a; }
 
 __device__ __forceinline__ double shfl_xor_d(double v, int m, unsigned mask = 0xffffffffu) {
     return __shfl_xor_sync(mask, v, m);

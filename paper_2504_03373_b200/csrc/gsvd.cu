@@ -1116,7 +1116,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
         }
     };
     if (tid == 0) clk0 = clock64();
-    form_whitened(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W);
+    form_whitened_staged(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W, Y);
     mark(0);
     const bool precond = a.precondition && a.ascratch;
     double2* ag = precond ? a.ascratch + (size_t)blk * m * m : nullptr;

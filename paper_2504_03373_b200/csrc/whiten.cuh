@@ -12,8 +12,8 @@ constexpr int kWhitenBatch = 8;  // K^-1 loads in flight per thread
 // acc[u] += sum_k K^-1[i][k] R[k][j_u], K^-1 row i streamed from global in
 // batches of kWhitenBatch independent loads (the row is L2-resident; a
 // dependent load per k would serialize ~m L2 round trips per thread).
-template <typename ColFn>
-__device__ __forceinline__ void whiten_rows(const double2* __restrict__ krow, const float2* rs, int m, double2* acc,
+template <typename RT, typename ColFn>
+__device__ __forceinline__ void whiten_rows(const double2* __restrict__ krow, const RT* rs, int m, int ld, double2* acc,
                                             ColFn col) {
     for (int k0 = 0; k0 < m; k0 += kWhitenBatch) {
         double2 kv[kWhitenBatch];
@@ -27,7 +27,7 @@ __device__ __forceinline__ void whiten_rows(const double2* __restrict__ krow, co
                 for (int u = 0; u < 8; ++u) {
                     const int j = col(u);
                     if (j >= 0) {
-                        const double2 r = f2d(rs[k * m + j]);
+                        const double2 r = f2d(rs[k * ld + j]);
                         acc[u].x = fma(kv[b].x, r.x, fma(-kv[b].y, r.y, acc[u].x));
                         acc[u].y = fma(kv[b].x, r.y, fma(kv[b].y, r.x, acc[u].y));
                     }
@@ -61,7 +61,7 @@ __device__ __forceinline__ void form_whitened(const float2* __restrict__ rb, con
             double2 acc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[u] = make_double2(0, 0);
-            whiten_rows(krow, rs, m, acc, [&](int u) {
+            whiten_rows(krow, rs, m, m, acc, [&](int u) {
                 const int j = j0 + u * parts;
                 return j < jl ? j : -1;
             });
@@ -77,7 +77,7 @@ __device__ __forceinline__ void form_whitened(const float2* __restrict__ rb, con
 #pragma unroll
     for (int u = 0; u < 8; ++u) hold[u] = make_double2(0, 0);
     if (active)
-        whiten_rows(krow, rs, m, hold, [&](int u) {
+        whiten_rows(krow, rs, m, m, hold, [&](int u) {
             const int j = jl + part + u * parts;
             return j < m ? j : -1;
         });
@@ -90,6 +90,46 @@ __device__ __forceinline__ void form_whitened(const float2* __restrict__ rb, con
         }
     }
     __syncthreads();
+}
+
+// A = K^-1 R into W with R widened to FP64 once, one column half at a time,
+// in a separate buffer `stage` (>= m * ceil(m/2) entries): the inner loop is
+// one 16-byte shared load per complex MAC instead of a load and two
+// conversions, and W is written directly.  Bit-identical to form_whitened.
+__device__ __forceinline__ void form_whitened_staged(const float2* __restrict__ rb, const double2* __restrict__ kb,
+                                                     int m, double2* W, double2* stage) {
+    const int tid = threadIdx.x;
+    const int nt = blockDim.x;
+    int parts = nt / m;
+    if (parts > m) parts = m;
+    const bool active = tid < m * parts;
+    const int i = active ? tid / parts : 0;
+    const int part = active ? tid % parts : 0;
+    const double2* krow = kb + (size_t)i * m;
+    const int jh = (m + 1) / 2;
+    for (int h = 0; h < 2; ++h) {
+        const int j0 = h ? jh : 0, nj = h ? m - jh : jh;
+        for (int e = tid; e < m * nj; e += nt) {
+            const int k = e / nj, jj = e - k * nj;
+            stage[e] = f2d(rb[k * m + j0 + jj]);
+        }
+        __syncthreads();
+        if (active && nj > 0) {
+            double2 acc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[u] = make_double2(0, 0);
+            whiten_rows(krow, stage, m, nj, acc, [&](int u) {
+                const int jj = part + u * parts;
+                return jj < nj ? jj : -1;
+            });
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int jj = part + u * parts;
+                if (jj < nj) W[(j0 + jj) * m + i] = acc[u];
+            }
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace sslg
