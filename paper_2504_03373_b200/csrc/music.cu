@@ -290,7 +290,10 @@ void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
         const int nchunk = (a.dirs + chunk - 1) / chunk;
         kern<<<nblk * a.bins * nchunk, 16 * dt, smem2, s>>>(a, nblk, nchunk);
     };
-    if (a.m - a.ns <= kNPad) {  // register-tiled kernel
+    // register-tiled kernel: 16 slices of 4 noise vectors per direction, so
+    // it needs enough noise vectors to fill them (C1/C2, with 6 and 14, run
+    // 3.5x faster on the generic kernel)
+    if (a.m - a.ns <= kNPad && a.m - a.ns >= 32) {
         if (a.dirs >= 256) {
             tiled(spectrum_tiled_kernel<16>, 16);
             return;
