@@ -437,3 +437,29 @@ def test_vanishing_block_with_rejected_candidates(port, rank):
     assert np.all(conv)
     assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
     assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, rank
+
+
+@pytest.mark.parametrize("tied", [12, 30])
+def test_tied_groups_against_oracle(port, tied):
+    """Runs of equal singular values (tied groups, gsvd.cpp:505-543): a group
+    of 12 takes the fused coordinate-space picker, a group of 30 (> kZMax)
+    the generic canonical_kernel; both must match the oracle's vectors."""
+    from paper_2504_03373_b200 import ssl
+
+    m, bins = 60, 2
+    rng = np.random.default_rng(300 + tied)
+    s = np.concatenate([np.linspace(9.0, 5.0, 10), np.full(tied, 2.0), np.linspace(1.5, 0.5, m - 10 - tied)])
+    r = np.empty((bins, m, m), np.complex64)
+    for b in range(bins):
+        q, _ = np.linalg.qr(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m)))
+        r[b] = (q * s) @ q.conj().T
+    k = np.broadcast_to(np.eye(m, dtype=np.complex64), (bins, m, m)).copy()
+    eng = ssl.Engine(m, bins, window_frames=2, max_batch=2)
+    eng.set_noise_model(k)
+    sigma, e, _, conv = eng.gsvd(r)
+    eng.close()
+    want = port.gsvd_reference(k, r, threads=4)
+    smax = want["sigma"][:, :1]
+    assert np.all(conv)
+    assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+    assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, tied
