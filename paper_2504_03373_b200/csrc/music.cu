@@ -83,104 +83,117 @@ __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
 }
 
 
-// Register-tiled variant for large grids (C4: 1368 directions): each thread
-// owns a 4-direction x 4-vector tile of h^H e products, so one mic step loads
-// 4 steering + 4 noise values for 16 complex MACs (64 FP64 FMAs).  The noise
-// vectors are staged transposed ([mic][vector], padded to 64) and the
-// steering chunk as [mic][direction], so a warp's loads are contiguous and
-// conflict-free.  The 16 threads holding the same directions and different
-// vector slices are adjacent lanes; their partial denominators meet in a
-// 4-level shuffle tree, identical for every direction (exact ties survive).
-constexpr int kTileD = 4, kTileN = 4, kSlices = 16;
-constexpr int kNPad = kTileN * kSlices;      // 64 vector slots
-constexpr int kEStride = kNPad + 1;          // double2 row stride of the staged noise vectors (bank spread)
+// FP64 tensor-core variant (DMMA, mma.sync m8n8k4 .f64), used whenever the
+// noise subspace has 16..64 vectors (C3, C4; C1/C2 keep the kernel above):
+// the contraction
+// h^H e for a warp's 8 directions x 64 noise-vector slots is 8 complex 8x8
+// tiles, each k-step of 4 mics four real MMAs (Re += Hr Er + Hi Ei,
+// Im += Hr Ei - Hi Er).  One instruction carries 256 FMAs, so the issue
+// overhead of an FFMA-tiled kernel (loads, conversions, index math per
+// 4 FMAs) disappears; B200 runs DMMA at 37 TFLOP/s vs 33 for DFMA
+// (tools/ubench/dmma.cu).  Fragment layouts (PTX m8n8k4 .f64): A[r][c] at
+// lane 4r + c, B[k][n] at lane 4n + k, C[r][2c + i] at lane 4r + c.  Every
+// direction's denominator is reduced in the same order (its lane's two
+// columns per tile over the tiles, then the 4 lanes of its row), so exact
+// steering ties stay exact.
+constexpr int kMmaN = 64;  // noise-vector slots (8 tiles of 8)
 
-// DT direction tiles of 4 per CTA (16 lanes each): 64 directions at DT = 16
-// (large grids), the whole 72-direction ring at DT = 18.
-template <int DT>
-__global__ void __launch_bounds__(16 * DT, 2) spectrum_tiled_kernel(SpecArgs a, int nblk, int nchunk) {
-    constexpr int kChunk2 = kTileD * DT;
-    constexpr int kHStride = kChunk2 + 2;  // float2 row stride of the staged steering (16-B aligned rows)
+__device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int mma_kpad(int m) { return (m + 3) & ~3; }
+// noise-vector row stride (double2): = 4 mod 8, so the two vectors a quarter
+// warp reads land in opposite bank halves
+__host__ __device__ inline int mma_estride(int m) { return ((mma_kpad(m) + 3) & ~7) + 4; }
+// steering row stride (float2): = 4 mod 16 (two rows per quarter warp)
+__host__ __device__ inline int mma_hstride(int m) { return ((mma_kpad(m) + 11) & ~15) + 4; }
+
+template <int WPC>
+__global__ void __launch_bounds__(32 * WPC, 2) spectrum_mma_kernel(SpecArgs a, int nblk) {
+    constexpr int kChunk = 8 * WPC;
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = a.m;
     const int nn = m - a.ns;
-    double2* Et = reinterpret_cast<double2*>(smem_raw);                 // [m][kEStride]
-    float2* Hs = reinterpret_cast<float2*>(Et + (size_t)m * kEStride);  // [m][kHStride]
-    // linear CTA index = (bin * nblk + block) * nchunk + chunk: the chunks of
-    // one (block, bin) run back to back (its noise vectors stay in L2) and
-    // the blocks of one bin follow each other (its steering stays in L2)
-    const int chunk = blockIdx.x % nchunk;
-    const int bb = blockIdx.x / nchunk;
-    const int bin = bb / nblk, blk = bb % nblk;
+    const int kp = mma_kpad(m), es = mma_estride(m), hs = mma_hstride(m);
+    double2* Es = reinterpret_cast<double2*>(smem_raw);                 // [kMmaN][es]
+    float2* Hs = reinterpret_cast<float2*>(Es + (size_t)kMmaN * es);  // [kChunk][hs]
+    // one CTA per (bin, block), blocks of a bin adjacent (its steering stays
+    // in L2); the noise vectors are staged once and every direction chunk of
+    // the grid streams past them
+    const int bin = blockIdx.x / nblk, blk = blockIdx.x % nblk;
     const int blkbin = blk * a.bins + bin;
-    const int d0 = chunk * kChunk2;
-    const int nd = min(kChunk2, a.dirs - d0);
     const int t = threadIdx.x;
 
-    // staging: coalesced global reads, transposed shared writes (padded strides)
     const double2* eb = a.e + ((size_t)blkbin * m + a.ns) * m;  // [nn][m]
-    for (int x = t; x < kNPad * m; x += blockDim.x) {
-        const int v = x / m, mic = x % m;
-        Et[mic * kEStride + v] = v < nn ? eb[(size_t)v * m + mic] : make_double2(0, 0);
+    for (int x = t; x < kMmaN * kp; x += blockDim.x) {
+        const int v = x / kp, mic = x - v * kp;
+        Es[v * es + mic] = (v < nn && mic < m) ? eb[(size_t)v * m + mic] : make_double2(0, 0);
     }
-    const float2* hb = a.h + ((size_t)bin * a.dirs + d0) * m;
-    for (int x = t; x < kChunk2 * m; x += blockDim.x) {
-        const int d = x / m, mic = x % m;
-        Hs[mic * kHStride + d] = d < nd ? hb[(size_t)d * m + mic] : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-
-    const int slice = t % kSlices, dtile = t / kSlices;
-    double2 acc[kTileD][kTileN];
-#pragma unroll
-    for (int i = 0; i < kTileD; ++i)
-#pragma unroll
-        for (int j = 0; j < kTileN; ++j) acc[i][j] = make_double2(0, 0);
-    const float2* hrow = Hs + dtile * kTileD;
-    const double2* erow = Et + slice;  // vectors slice, slice + 16, ...: lanes read consecutive 16 B
-#pragma unroll 2
-    for (int mic = 0; mic < m; ++mic) {
-        const float4 h01 = *reinterpret_cast<const float4*>(hrow + mic * kHStride);
-        const float4 h23 = *reinterpret_cast<const float4*>(hrow + mic * kHStride + 2);
-        const double2 h[kTileD] = {make_double2(h01.x, h01.y), make_double2(h01.z, h01.w),
-                                   make_double2(h23.x, h23.y), make_double2(h23.z, h23.w)};
-        double2 e[kTileN];
-#pragma unroll
-        for (int j = 0; j < kTileN; ++j) e[j] = erow[mic * kEStride + j * kSlices];
-#pragma unroll
-        for (int i = 0; i < kTileD; ++i)
-#pragma unroll
-            for (int j = 0; j < kTileN; ++j) {  // conj(h) e
-                acc[i][j].x = fma(h[i].x, e[j].x, fma(h[i].y, e[j].y, acc[i][j].x));
-                acc[i][j].y = fma(h[i].x, e[j].y, fma(-h[i].y, e[j].x, acc[i][j].y));
-            }
-    }
-    double den[kTileD];
-#pragma unroll
-    for (int i = 0; i < kTileD; ++i) {
-        double sum = 0;
-#pragma unroll
-        for (int j = 0; j < kTileN; ++j) {
-            const double mag = hypot(acc[i][j].x, acc[i][j].y);
-            sum += a.squared ? mag * mag : mag;
+    const int warp = t >> 5, lane = t & 31;
+    const int r = lane >> 2, c = lane & 3;
+    const int nchunk = (a.dirs + kChunk - 1) / kChunk;
+    float2* Hw = Hs + warp * 8 * hs;  // this warp's 8 steering rows (warp-private)
+    __syncthreads();                  // the noise vectors are staged
+    for (int chunk = 0; chunk < nchunk; ++chunk) {
+        const int d0 = chunk * kChunk;
+        const int nd = min(kChunk, a.dirs - d0);
+        // each warp stages its own 8 directions: no block barrier per chunk
+        __syncwarp();  // the previous chunk's rows are consumed
+        const int dw = d0 + warp * 8;
+        const float2* hb = a.h + ((size_t)bin * a.dirs + dw) * m;
+        for (int x = lane; x < 8 * kp; x += 32) {
+            const int d = x / kp, mic = x - d * kp;
+            Hw[d * hs + mic] = (dw + d < a.dirs && warp * 8 + d < nd && mic < m) ? hb[(size_t)d * m + mic]
+                                                                               : make_float2(0.f, 0.f);
         }
-        den[i] = sum;
-    }
+        __syncwarp();
+
+        const float2* hrow = Hs + (warp * 8 + r) * hs + c;  // A[r][c] = h(dir r, mic k0 + c)
+        double den = 0.0;
+        // two passes of 4 vector tiles (32 accumulator registers each)
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            const double2* ecol = Es + (half * 32 + r) * es + c;  // B[c][r] = e(vector 8j + r, mic k0 + c)
+            double re[4][2], im[4][2];
 #pragma unroll
-    for (int o = kSlices / 2; o > 0; o >>= 1)
+            for (int j = 0; j < 4; ++j) re[j][0] = re[j][1] = im[j][0] = im[j][1] = 0.0;
+            for (int k0 = 0; k0 < kp; k0 += 4) {
+                const float2 hv = hrow[k0];
+                const double hr = hv.x, hi = hv.y, nhi = -hi;
+                double2 ev[4];
 #pragma unroll
-        for (int i = 0; i < kTileD; ++i) den[i] += __shfl_xor_sync(0xffffffffu, den[i], o);
-    if (slice < kTileD) {
-        const int d = dtile * kTileD + slice;
-        double dd = den[0];
+                for (int j = 0; j < 4; ++j) ev[j] = ecol[j * 8 * es + k0];
+                // 8 independent accumulators between two updates of the same one
 #pragma unroll
-        for (int i = 1; i < kTileD; ++i)
-            if (slice == i) dd = den[i];
-        if (d < nd) {
-            if (dd < a.floor_) dd = a.floor_;
+                for (int j = 0; j < 4; ++j) {
+                    dmma8x8x4(re[j][0], re[j][1], hr, ev[j].x);
+                    dmma8x8x4(im[j][0], im[j][1], hr, ev[j].y);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    dmma8x8x4(re[j][0], re[j][1], hi, ev[j].y);
+                    dmma8x8x4(im[j][0], im[j][1], nhi, ev[j].x);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double mag = hypot(re[j][i], im[j][i]);  // 0 on padded vectors
+                    den += a.squared ? mag * mag : mag;
+                }
+        }
+        den += __shfl_xor_sync(0xffffffffu, den, 1);
+        den += __shfl_xor_sync(0xffffffffu, den, 2);
+        const int d = warp * 8 + r;
+        if (c == 0 && d < nd) {
+            if (den < a.floor_) den = a.floor_;
             const double num = a.num[(size_t)bin * a.dirs + d0 + d];
-            a.p[(size_t)blkbin * a.dirs + d0 + d] = num / dd;
+            a.p[(size_t)blkbin * a.dirs + d0 + d] = num / den;
         }
     }
 }
@@ -283,25 +296,17 @@ void spectrum_shape(int m, int ns, int dirs, int& dchunk, int& nsplit, size_t& s
 }
 
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
-    auto tiled = [&](auto kern, int dt) {
-        const int chunk = kTileD * dt;
-        const size_t smem2 = (size_t)a.m * kEStride * sizeof(double2) + (size_t)a.m * (chunk + 2) * sizeof(float2);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        const int nchunk = (a.dirs + chunk - 1) / chunk;
-        kern<<<nblk * a.bins * nchunk, 16 * dt, smem2, s>>>(a, nblk, nchunk);
-    };
-    // register-tiled kernel: 16 slices of 4 noise vectors per direction, so
-    // it needs enough noise vectors to fill them (C1/C2, with 6 and 14, run
-    // 3.5x faster on the generic kernel)
-    if (a.m - a.ns <= kNPad && a.m - a.ns >= 32) {
-        if (a.dirs >= 256) {
-            tiled(spectrum_tiled_kernel<16>, 16);
-            return;
-        }
-        if (a.dirs > 64 && a.dirs <= 72) {
-            tiled(spectrum_tiled_kernel<18>, 18);
-            return;
-        }
+    if (a.m - a.ns <= kMmaN && a.m - a.ns >= 16) {  // FP64 tensor cores
+        auto mma = [&](auto kern, int wpc) {
+            const int chunk = 8 * wpc;
+            const size_t smem2 = (size_t)kMmaN * mma_estride(a.m) * sizeof(double2) +
+                                 (size_t)chunk * mma_hstride(a.m) * sizeof(float2);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+            kern<<<nblk * a.bins, 32 * wpc, smem2, s>>>(a, nblk);
+        };
+        if (a.dirs % 72 == 0) mma(spectrum_mma_kernel<9>, 9);
+        else mma(spectrum_mma_kernel<8>, 8);
+        return;
     }
     size_t smem;
     spectrum_shape(a.m, a.ns, a.dirs, a.dchunk, a.nsplit, smem);

@@ -16,14 +16,14 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --batch 8 --no-cpu-baseline --no-flush > gpurun_out/ncu_launch.log 2>&1
   echo "ncu launches rc=$?"
-  for K in ${NCU_KERNELS:-jacobi_kernel spectrum_kernel correlation_kernel stft_kernel canonical_kernel}; do
+  for K in ${NCU_KERNELS:-jacobi_kernel spectrum_mma_kernel correlation_kernel stft_kernel canonical_kernel}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 \
       -o gpurun_out/prof_$K -f python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-flush \
       > gpurun_out/ncu_$K.log 2>&1
     echo "ncu $K rc=$?"
   done
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:spectrum_tiled -s 1 -c 1 \
-    -o gpurun_out/prof_spectrum_tiled_kernel -f python bench.py --config c4 --steps 1 --warmup 1 --batch 8 \
-    --no-cpu-baseline --no-flush > gpurun_out/ncu_spectrum_tiled.log 2>&1
-  echo "ncu spectrum_tiled rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:spectrum_mma -s 1 -c 1 \
+    -o gpurun_out/prof_spectrum_mma_c4 -f python bench.py --config c4 --steps 1 --warmup 1 --batch 8 \
+    --no-cpu-baseline --no-flush > gpurun_out/ncu_spectrum_mma_c4.log 2>&1
+  echo "ncu spectrum_mma c4 rc=$?"
 fi
