@@ -463,3 +463,26 @@ def test_tied_groups_against_oracle(port, tied):
     assert np.all(conv)
     assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
     assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, tied
+
+
+@pytest.mark.parametrize("m,ns", [(37, 2), (64, 3), (20, 4)])
+def test_tensor_core_spectrum_against_oracle(port, m, ns):
+    """The DMMA spectrum kernel (16..64 noise vectors) at channel counts that
+    are not multiples of 4 and at the 64-channel maximum, on a direction count
+    that is not a multiple of the 8-direction tile, against the oracle's
+    calc_average_power (music.cpp:112-165): 1e-9 relative per bin."""
+    from paper_2504_03373_b200 import ssl
+
+    rng = np.random.default_rng(900 + m)
+    bins, dirs = 3, 77
+    q, _ = np.linalg.qr(rng.standard_normal((bins, m, m)) + 1j * rng.standard_normal((bins, m, m)))
+    e = q.astype(np.complex128)
+    h = (rng.standard_normal((dirs, bins, m)) + 1j * rng.standard_normal((dirs, bins, m))).astype(np.complex64)
+    steer = ssl.SteeringField(m, 0, bins - 1, np.zeros((dirs, 2)), h)
+    basis = ssl.GsvdBatch(np.ones((bins, m)), e, np.zeros(bins), np.ones(bins, bool))
+    for squared in (False, True):
+        cfg = ssl.MusicConfig(num_sources=ns, squared_denominator=squared)
+        got = ssl.calc_average_power(basis, steer, cfg, keep_bins=True)
+        want_p, want_bp = port.spectrum(e, h, ns, squared=squared, keep_bins=True)
+        assert np.max(np.abs(got.bin_power - want_bp) / want_bp) <= 1e-9
+        assert np.max(np.abs(got.power - want_p) / want_p) <= 1e-9
