@@ -24,6 +24,7 @@ namespace sslg {
 
 constexpr int kCorrThreads = 512;
 constexpr int kCorrPer = (kMaxM * kMaxM + kCorrThreads - 1) / kCorrThreads;  // 8
+constexpr int kCorrChunk = 32;  // frames staged per pass
 
 __device__ __forceinline__ void outer_acc(double2& acc, float2 xi, float2 xj, bool subtract) {
     const double a = xi.x, b = xi.y, c = xj.x, d = xj.y;
@@ -39,22 +40,22 @@ __device__ __forceinline__ void outer_acc(double2& acc, float2 xi, float2 xj, bo
     }
 }
 
-__global__ void __launch_bounds__(kCorrThreads) correlation_kernel(CorrArgs a) {
+__global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a) {
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     __shared__ float2 xs_new[kMaxM];
-    __shared__ float2 xs_old[kMaxM];
+    __shared__ float2 xc_new[kCorrChunk * kMaxM];
+    __shared__ float2 xc_old[kCorrChunk * kMaxM];
     const int b = blockIdx.x;
     const int m = a.m;
     const int mm = m * m;
     const int tid = threadIdx.x;
 
     double2 acc[kCorrPer];
-    int ei[kCorrPer], ej[kCorrPer];
+    int eij[kCorrPer];  // (row << 8) | column of each owned entry
 #pragma unroll
     for (int k = 0; k < kCorrPer; ++k) {
         const int e = tid + k * kCorrThreads;
-        ei[k] = e / m;
-        ej[k] = e % m;
+        eij[k] = ((e / m) << 8) | (e % m);
         acc[k] = e < mm ? a.state[(size_t)b * mm + e] : make_double2(0, 0);
     }
     const double inv_t = 1.0 / (double)a.t;
@@ -65,45 +66,57 @@ __global__ void __launch_bounds__(kCorrThreads) correlation_kernel(CorrArgs a) {
 
     auto frame_ptr = [&](long long g) { return a.ring + (size_t)(g % a.cap) * m * a.bins; };
 
-    for (int f = 0; f < a.frames; ++f) {
-        const long long g = a.pushed0 + f;
-        const bool drop_old = pushed >= a.t;
+    // the bin's entering and leaving frame values for up to kCorrChunk frames
+    // are staged together up front, so the sequential recurrence below never
+    // waits on a global load
+    for (int f0 = 0; f0 < a.frames; f0 += kCorrChunk) {
+        const int nf = min(kCorrChunk, a.frames - f0);
         __syncthreads();
-        if (tid < m) xs_new[tid] = frame_ptr(g)[(size_t)tid * a.bins + b];
-        else if (drop_old && tid < 2 * m) xs_old[tid - m] = frame_ptr(g - a.t)[(size_t)(tid - m) * a.bins + b];
+        for (int x = tid; x < nf * m; x += kCorrThreads) {
+            const int fi = x / m, ch = x - fi * m;
+            const long long g = a.pushed0 + f0 + fi;
+            xc_new[x] = frame_ptr(g)[(size_t)ch * a.bins + b];
+            if (g >= a.t) xc_old[x] = frame_ptr(g - a.t)[(size_t)ch * a.bins + b];
+        }
         __syncthreads();
-#pragma unroll
-        for (int k = 0; k < kCorrPer; ++k) {
-            if (tid + k * kCorrThreads < mm) {
-                if (drop_old) outer_acc(acc[k], xs_old[ei[k]], xs_old[ej[k]], true);
-                outer_acc(acc[k], xs_new[ei[k]], xs_new[ej[k]], false);
-            }
-        }
-        ++pushed;
-        if (++since >= a.rebuild_interval) {
-            // rebuild oldest first (correlation.cpp:75-84)
-            const long long have = pushed < a.t ? pushed : a.t;
-#pragma unroll
-            for (int k = 0; k < kCorrPer; ++k) acc[k] = make_double2(0, 0);
-            for (long long kk = 0; kk < have; ++kk) {
-                const long long gg = pushed - have + kk;
-                __syncthreads();
-                if (tid < m) xs_new[tid] = frame_ptr(gg)[(size_t)tid * a.bins + b];
-                __syncthreads();
-#pragma unroll
-                for (int k = 0; k < kCorrPer; ++k)
-                    if (tid + k * kCorrThreads < mm) outer_acc(acc[k], xs_new[ei[k]], xs_new[ej[k]], false);
-            }
-            since = 0;
-        }
-        if (f >= first_emit) {
-            float2* r = a.r_out + ((size_t)(f - first_emit) * a.bins + b) * mm;
+        for (int fi = 0; fi < nf; ++fi) {
+            const int f = f0 + fi;
+            const bool drop_old = pushed >= a.t;
+            const float2* xn = xc_new + fi * m;
+            const float2* xo = xc_old + fi * m;
 #pragma unroll
             for (int k = 0; k < kCorrPer; ++k) {
-                const int e = tid + k * kCorrThreads;
-                if (e < mm)
-                    r[e] = make_float2(__double2float_rn(__dmul_rn(acc[k].x, inv_t)),
-                                       __double2float_rn(__dmul_rn(acc[k].y, inv_t)));
+                if (tid + k * kCorrThreads < mm) {
+                    if (drop_old) outer_acc(acc[k], xo[eij[k] >> 8], xo[eij[k] & 255], true);
+                    outer_acc(acc[k], xn[eij[k] >> 8], xn[eij[k] & 255], false);
+                }
+            }
+            ++pushed;
+            if (++since >= a.rebuild_interval) {
+                // rebuild oldest first (correlation.cpp:75-84)
+                const long long have = pushed < a.t ? pushed : a.t;
+#pragma unroll
+                for (int k = 0; k < kCorrPer; ++k) acc[k] = make_double2(0, 0);
+                for (long long kk = 0; kk < have; ++kk) {
+                    const long long gg = pushed - have + kk;
+                    __syncthreads();
+                    if (tid < m) xs_new[tid] = frame_ptr(gg)[(size_t)tid * a.bins + b];
+                    __syncthreads();
+#pragma unroll
+                    for (int k = 0; k < kCorrPer; ++k)
+                        if (tid + k * kCorrThreads < mm) outer_acc(acc[k], xs_new[eij[k] >> 8], xs_new[eij[k] & 255], false);
+                }
+                since = 0;
+            }
+            if (f >= first_emit) {
+                float2* r = a.r_out + ((size_t)(f - first_emit) * a.bins + b) * mm;
+#pragma unroll
+                for (int k = 0; k < kCorrPer; ++k) {
+                    const int e = tid + k * kCorrThreads;
+                    if (e < mm)
+                        r[e] = make_float2(__double2float_rn(__dmul_rn(acc[k].x, inv_t)),
+                                           __double2float_rn(__dmul_rn(acc[k].y, inv_t)));
+                }
             }
         }
     }
