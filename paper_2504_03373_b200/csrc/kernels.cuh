@@ -93,7 +93,8 @@ struct PeakArgs {
     int bins, dirs, ns;
     double low_ratio;         // double(float ratio)
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
+    int peak_chunk = 1;                   // bins staged per pass (set by launch_peaks)
 };
-void launch_peaks(const PeakArgs& a, int nblk, cudaStream_t s);
+void launch_peaks(PeakArgs a, int nblk, cudaStream_t s);
 
 }  // namespace sslg

@@ -218,7 +218,7 @@ __global__ void steering_prep_kernel(const float2* __restrict__ h_in,  // [dirs]
     num[idx] = acc;
 }
 
-constexpr int kPeakThreads = 256;
+constexpr int kPeakThreads = 512;
 
 __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs a) {
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
@@ -229,12 +229,43 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
     const int blk = blockIdx.x;
     const int t = threadIdx.x;
     const double* pb = a.p + (size_t)blk * a.bins * a.dirs;
-    for (int d = t; d < a.dirs; d += blockDim.x) {
-        double acc = 0.0;
-        for (int b = 0; b < a.bins; ++b) acc = __dadd_rn(acc, pb[(size_t)b * a.dirs + d]);
-        pw[d] = acc;
-        a.power[(size_t)blk * a.dirs + d] = acc;
+    // ascending-bin FP64 sum per direction (music.cpp:160)
+    if (a.peak_chunk > 1) {
+        // small grids: chunks of cb bins ([cb][dirs], contiguous in P) are
+        // staged by the whole CTA with coalesced loads, then every
+        // direction's running sum walks its column
+        double* stage = reinterpret_cast<double*>(is_peak + a.dirs + (a.dirs & 1));  // [cb][dirs]
+        const int cb = a.peak_chunk;
+        for (int d = t; d < a.dirs; d += blockDim.x) pw[d] = 0.0;
+        for (int b0 = 0; b0 < a.bins; b0 += cb) {
+            const int nb = min(cb, a.bins - b0);
+            __syncthreads();
+            const double* src = pb + (size_t)b0 * a.dirs;
+            for (int x = t; x < nb * a.dirs; x += blockDim.x) stage[x] = src[x];
+            __syncthreads();
+            for (int d = t; d < a.dirs; d += blockDim.x) {
+                double acc = pw[d];
+                for (int u = 0; u < nb; ++u) acc = __dadd_rn(acc, stage[u * a.dirs + d]);
+                pw[d] = acc;
+            }
+        }
+    } else {
+        // large grids: a thread per direction, 16 bins' loads in flight
+        for (int d = t; d < a.dirs; d += blockDim.x) {
+            double acc = 0.0;
+            int b = 0;
+            for (; b + 16 <= a.bins; b += 16) {
+                double v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = pb[(size_t)(b + u) * a.dirs + d];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, v[u]);
+            }
+            for (; b < a.bins; ++b) acc = __dadd_rn(acc, pb[(size_t)b * a.dirs + d]);
+            pw[d] = acc;
+        }
     }
+    for (int d = t; d < a.dirs; d += blockDim.x) a.power[(size_t)blk * a.dirs + d] = pw[d];
     __syncthreads();
     if (t == 0) {
         double mean = 0;
@@ -243,12 +274,19 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
         s_mean = mean;
     }
     for (int d = t; d < a.dirs; d += blockDim.x) {
+        // local-maximum test over the CSR neighbor list, 8 neighbor indices
+        // loaded together per step (the list lives in global memory)
+        const double v = pw[d];
+        const uint32_t k1 = a.nbr_off[d + 1];
         int ok = 1;
-        for (uint32_t k = a.nbr_off[d]; k < a.nbr_off[d + 1]; ++k)
-            if (pw[d] < pw[a.nbr[k]]) {
-                ok = 0;
-                break;
-            }
+        for (uint32_t k = a.nbr_off[d]; k < k1 && ok; k += 8) {
+            uint32_t nb[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nb[u] = k + u < k1 ? a.nbr[k + u] : (uint32_t)d;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v < pw[nb[u]]) ok = 0;
+        }
         is_peak[d] = ok;
     }
     __syncthreads();
@@ -321,8 +359,13 @@ void launch_steering_prep(const float2* h_in, float2* h_t, double* num, int m, i
     steering_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h_in, h_t, num, m, bins, dirs);
 }
 
-void launch_peaks(const PeakArgs& a, int nblk, cudaStream_t s) {
-    const size_t smem = (size_t)a.dirs * (sizeof(double) + sizeof(int));
+void launch_peaks(PeakArgs a, int nblk, cudaStream_t s) {
+    // small grids stage ~40 KB of P per pass (>= 16 bins); large ones read directly
+    a.peak_chunk = (int)(40960 / ((size_t)a.dirs * sizeof(double)));
+    if (a.peak_chunk < 16) a.peak_chunk = 1;
+    if (a.peak_chunk > a.bins) a.peak_chunk = a.bins;
+    const size_t smem = (size_t)a.dirs * sizeof(double) + (size_t)(a.dirs + (a.dirs & 1)) * sizeof(int) +
+                        (size_t)a.peak_chunk * a.dirs * sizeof(double);
     cudaFuncSetAttribute(integrate_peaks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     integrate_peaks_kernel<<<nblk, kPeakThreads, smem, s>>>(a);
 }
