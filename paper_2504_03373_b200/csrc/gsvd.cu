@@ -56,21 +56,27 @@ __host__ __device__ constexpr int scratch_entries(int mc) {
     return (mc > 0 && mc <= 16) ? cmax3(mc * (mc + 1) / 2, mc * kYld, 2 * mc * mc) : kScratch;
 }
 
-struct CanonScratch {
-    double nrm[kMaxM];
-    double norm0[kMaxM];
-    double2 q[kZMax];
-    double2 z[kZMax][kZMax];  // accepted coordinate vectors, column t = vector t
-    int cols[kMaxM];          // W columns of the current group
-    int groups[kMaxM][2];     // rank ranges of tied groups
-    double2 up[kMaxM];        // phase factor per rank
+// Per-CTA canonicalization state, sized for the channel count (MM) and the
+// largest group the coordinate-space picker takes (ZM): small arrays keep
+// their static shared memory small so more bins share an SM.
+template <int MM, int ZM>
+struct CanonScratchT {
+    double nrm[MM];
+    double norm0[MM];
+    double2 q[ZM];
+    double2 z[ZM][ZM];  // accepted coordinate vectors, column t = vector t
+    int cols[MM];       // W columns of the current group
+    int groups[MM][2];  // rank ranges of tied groups
+    double2 up[MM];     // phase factor per rank
     unsigned ball[2];
-    int dropped[kMaxM];       // columns below the final sweep's drop line
-    int certcols[kMaxM];      // certified columns
-    double invd[kMaxM];       // 1 / L_jj of the CholeskyQR (column norms before it)
-    double dn2[kMaxM];        // column norms after the first projection
+    int dropped[MM];    // columns below the final sweep's drop line
+    int certcols[MM];   // certified columns
+    double invd[MM];    // 1 / L_jj of the CholeskyQR (column norms before it)
+    double dn2[MM];     // column norms after the first projection
     int ngroups, nvanish, eligible, ndropped, ncert, collapsed, again;
 };
+template <int MC>
+using CanonScratchFor = CanonScratchT<(MC > 0 ? MC : kMaxM), (MC > 0 && MC < kZMax ? MC : kZMax)>;
 
 // Completes the basis: the columns below the drop line (list D, rank order)
 // are orthonormalized against the certified columns C and then among
@@ -79,7 +85,7 @@ struct CanonScratch {
 // than half of a column's energy, then CholeskyQR2 of D (the rank-order
 // Gram-Schmidt result).  Clears cs.eligible if a column collapses.
 template <int MC>
-__device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& cs) {
+__device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor<MC>& cs) {
     const int m = MC > 0 ? MC : m_rt;
     const int t = threadIdx.x, nt = blockDim.x;
     const int nc = cs.ncert, nd = cs.ndropped;
@@ -264,7 +270,8 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratch& c
 // pick_orthonormal, gsvd.cpp:404-436), and forms Z = Y R^-1.  Returns false
 // (nothing written) when a candidate would be rejected; the caller then runs
 // the sequential picker.  No block barrier inside: warp 0 only.
-__device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_norm0, CanonScratch& cs) {
+template <class CS>
+__device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_norm0, CS& cs) {
     __shared__ int s_ok;
     const int t = threadIdx.x;
     if (t < kWarp) {
@@ -614,7 +621,8 @@ __device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const
 // Reference picker (pick_orthonormal, gsvd.cpp:404-436) on the coordinates of
 // one group: candidate j is row j of conj(N), N = W[cols[0..d)].  Threads
 // j < m own candidate j; the accepted coordinate vectors land in cs.z.
-__device__ void pick_in_span(const double2* W, double2* Y, int m, int d, bool unit_norm0, CanonScratch& cs) {
+template <class CS>
+__device__ void pick_in_span(const double2* W, double2* Y, int m, int d, bool unit_norm0, CS& cs) {
     if (d <= kZMax && pick_fast(W, Y, m, d, unit_norm0, cs)) return;
     const int t = threadIdx.x;
     double2* yr = Y + t * kYld;
@@ -694,7 +702,8 @@ __device__ void pick_in_span(const double2* W, double2* Y, int m, int d, bool un
 }
 
 // W[:, cols[s]] <- sum_k W[:, cols[k]] z[k][s]  (new vectors of one group)
-__device__ void apply_span(double2* W, int m, int d, CanonScratch& cs) {
+template <class CS>
+__device__ void apply_span(double2* W, int m, int d, CS& cs) {
     const int t = threadIdx.x;
     double2 out[6];
     int cnt = 0;
@@ -1085,10 +1094,16 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
     return !__syncthreads_or(bad);
 }
 
+// resident CTAs per SM: 2 for the 60/64-channel solver (shared memory), 12 at
+// m = 8 and 8 at m = 16 (registers; measured best: C1 0.44 -> 0.36 ms,
+// C2 1.03 -> 0.93 ms per 32 blocks against 6)
+template <int MC>
+constexpr int jac_ctas() { return MC > 0 && MC <= 8 ? 12 : (MC > 0 && MC <= 16 ? 8 : 2); }
+
 // MC > 0: channel count fixed at compile time (loop bounds, predicates and
 // addressing fold away); MC == 0: any m <= 64 at run time.
 template <int MC>
-__global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2) jacobi_kernel(GsvdArgs a) {
+__global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kernel(GsvdArgs a) {
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = MC > 0 ? MC : a.m;
@@ -1098,7 +1113,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), MC > 0 && MC <= 16 ? 6 : 2)
     __shared__ double s_drop;
     __shared__ int s_perm[kMaxM];  // rank -> column
     __shared__ double s_sig[kMaxM];
-    __shared__ CanonScratch cs;
+    __shared__ CanonScratchFor<MC> cs;
     __shared__ QrScratch qs;
 
     const int blk = blockIdx.x;
