@@ -108,8 +108,38 @@ __host__ __device__ inline int mma_kpad(int m) { return (m + 3) & ~3; }
 // noise-vector row stride (double2): = 4 mod 8, so the two vectors a quarter
 // warp reads land in opposite bank halves
 __host__ __device__ inline int mma_estride(int m) { return ((mma_kpad(m) + 3) & ~7) + 4; }
-// steering row stride (float2): = 4 mod 16 (two rows per quarter warp)
-__host__ __device__ inline int mma_hstride(int m) { return ((mma_kpad(m) + 11) & ~15) + 4; }
+// steering row stride (float2): = 4 or 12 mod 16 (two rows per quarter warp
+// in different banks); m itself when m = 4 mod 8 (bulk-copied rows)
+__host__ __device__ inline int mma_hstride(int m) { return (m & 7) == 4 ? m : ((mma_kpad(m) + 11) & ~15) + 4; }
+
+// 1-D bulk copies (TMA engine, cp.async.bulk) global -> shared, completed on
+// an mbarrier with a transaction byte count
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+}
 
 template <int WPC>
 __global__ void __launch_bounds__(32 * WPC, 2) spectrum_mma_kernel(SpecArgs a, int nblk) {
@@ -129,20 +159,46 @@ __global__ void __launch_bounds__(32 * WPC, 2) spectrum_mma_kernel(SpecArgs a, i
     const int t = threadIdx.x;
 
     const double2* eb = a.e + ((size_t)blkbin * m + a.ns) * m;  // [nn][m]
-    for (int x = t; x < kMmaN * kp; x += blockDim.x) {
-        const int v = x / kp, mic = x - v * kp;
-        Es[v * es + mic] = (v < nn && mic < m) ? eb[(size_t)v * m + mic] : make_double2(0, 0);
+    const int nchunk = (a.dirs + kChunk - 1) / kChunk;
+    // m = 4 mod 8: the staged layouts equal the global ones (row strides m),
+    // so the noise vectors — and the steering rows when one chunk covers the
+    // grid — arrive by bulk copy (one TMA request each) while the threads
+    // zero the padding rows
+    const bool bulk = (m & 7) == 4;
+    const bool hbulk = bulk && nchunk == 1;
+    __shared__ unsigned long long bar;
+    if (bulk) {
+        if (t == 0) mbar_init(&bar, 1);
+        __syncthreads();
+        const int nd0 = min(kChunk, a.dirs);
+        if (t == 0) {
+            const unsigned eb_bytes = (unsigned)(nn * m * sizeof(double2));
+            const unsigned hb_bytes = hbulk ? (unsigned)(nd0 * m * sizeof(float2)) : 0u;
+            mbar_expect_tx(&bar, eb_bytes + hb_bytes);
+            bulk_g2s(Es, eb, eb_bytes, &bar);
+            if (hbulk) bulk_g2s(Hs, a.h + (size_t)bin * a.dirs * m, hb_bytes, &bar);
+        }
+        for (int x = t; x < (kMmaN - nn) * m; x += blockDim.x) Es[nn * m + x] = make_double2(0, 0);
+        if (hbulk)
+            for (int x = t; x < (kChunk - nd0) * m; x += blockDim.x) Hs[nd0 * m + x] = make_float2(0.f, 0.f);
+        mbar_wait(&bar, 0);
+    } else {
+        for (int x = t; x < kMmaN * kp; x += blockDim.x) {
+            const int v = x / kp, mic = x - v * kp;
+            Es[v * es + mic] = (v < nn && mic < m) ? eb[(size_t)v * m + mic] : make_double2(0, 0);
+        }
     }
     const int warp = t >> 5, lane = t & 31;
     const int r = lane >> 2, c = lane & 3;
-    const int nchunk = (a.dirs + kChunk - 1) / kChunk;
     float2* Hw = Hs + warp * 8 * hs;  // this warp's 8 steering rows (warp-private)
-    __syncthreads();                  // the noise vectors are staged
+    __syncthreads();                  // the noise vectors (and padding) are staged
     for (int chunk = 0; chunk < nchunk; ++chunk) {
         const int d0 = chunk * kChunk;
         const int nd = min(kChunk, a.dirs - d0);
+        if (hbulk) goto compute;  // the steering rows came with the bulk copy
         // each warp stages its own 8 directions: no block barrier per chunk
         __syncwarp();  // the previous chunk's rows are consumed
+        {
         const int dw = d0 + warp * 8;
         const float2* hb = a.h + ((size_t)bin * a.dirs + dw) * m;
         for (int x = lane; x < 8 * kp; x += 32) {
@@ -151,7 +207,8 @@ __global__ void __launch_bounds__(32 * WPC, 2) spectrum_mma_kernel(SpecArgs a, i
                                                                                : make_float2(0.f, 0.f);
         }
         __syncwarp();
-
+        }
+    compute:
         const float2* hrow = Hs + (warp * 8 + r) * hs + c;  // A[r][c] = h(dir r, mic k0 + c)
         double den = 0.0;
         // two passes of 4 vector tiles (32 accumulator registers each)
