@@ -816,7 +816,6 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
                 mybeta = make_double2(-ph.x * alpha, -ph.y * alpha);
                 qs.u[k] = make_double2(x0.x + ph.x * alpha, x0.y + ph.y * alpha);
                 qs.tau = alpha > 0 ? fast_rcp(alpha * (alpha + ax0)) : 0.0;
-                qs.key[p] = 0u;
                 qs.piv[k] = p;
             }
             mypos = k;
@@ -885,6 +884,9 @@ __device__ void qrcp_to_rh(double2* W, int m, QrScratch& qs) {
 #pragma unroll
             for (int o = 1; o < QL; o <<= 1) nrm += __shfl_xor_sync(gmask, nrm, o);
             if (act && l == 0) qs.key[c] = pivot_key(nrm, c);
+            // the pivot leaves the key set only now: every warp read this
+            // step's keys before the barrier above
+            if (c == p && l == 0) qs.key[c] = 0u;
         }
         __syncthreads();
         if (c == p && l == k % QL) qs.u[k] = make_double2(0, 0);  // keep u zero above the next step
@@ -1229,6 +1231,9 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
                                 W[q * m + row] = Q[u];
                             }
                         }
+                        // lane 0 writes the norms the whole group loaded (one
+                        // converged LDS) before the group shuffles of the dot;
+                        // racecheck cannot see that ordering and warns
                         if (s == 0) {
                             cn[p] = cp;
                             cn[q] = cq;
