@@ -260,7 +260,93 @@ __global__ void __launch_bounds__(256, 2) sweep_bench(double2* out, int m, int s
     if (tid == 0) atomicAdd((unsigned long long*)clk, (unsigned long long)(t1 - t0));
     if (tid == 0) out[blockIdx.x] = make_double2(W[0].x + rots, mymax);
 }
+
+// 16-lane pair groups (4 rows per lane), 512 threads: the one-bin-per-SM
+// layout (MINB = 1, shared memory padded so only one CTA fits) against two
+// such CTAs per SM (MINB = 2, 64 registers)
+template <int MINB>
+__global__ void __launch_bounds__(512, MINB) sweep_bench16(double2* out, int m, int sweeps, long long* clk) {
+    constexpr int L = 16, R = 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* W = reinterpret_cast<double2*>(smem_raw);
+    __shared__ double cn[kMaxM];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+        unsigned h = (unsigned)(e * 2654435761u) ^ (unsigned)(blockIdx.x * 40503u);
+        W[e] = make_double2((h & 0xffff) / 65536.0 - 0.5, ((h >> 16) & 0xffff) / 65536.0 - 0.5);
+    }
+    if (tid < m) cn[tid] = 0;
+    __syncthreads();
+    const int g = tid / L, s = tid % L;
+    const int n_even = (m + 1) & ~1, npairs = n_even / 2;
+    for (int j = g * 2; j < g * 2 + 2 && j < m; ++j) {
+        double v = 0;
+        for (int u = 0; u < R; ++u) { const int row = s + u * L; if (row < m) v += cnorm(W[j * m + row]); }
+        v = group_sum<L>(v);
+        if (s == 0) cn[j] = v;
+    }
+    __syncthreads();
+    long long t0 = clock64();
+    double mymax = 0;
+    int rots = 0;
+    for (int sw = 0; sw < sweeps; ++sw) {
+        for (int r = 0; r < n_even - 1; ++r) {
+            if (g < npairs) {
+                int p, q;
+                rr_pair(r, g, n_even, p, q);
+                double2 P[R], Q[R];
+#pragma unroll
+                for (int u = 0; u < R; ++u) {
+                    const int row = s + u * L;
+                    P[u] = row < m ? W[p * m + row] : make_double2(0, 0);
+                    Q[u] = row < m ? W[q * m + row] : make_double2(0, 0);
+                }
+                double cp = cn[p], cq = cn[q];
+                if (rotate_pair<R, L>(P, Q, cp, cq, 0.0, s, m, mymax)) {
+                    ++rots;
+#pragma unroll
+                    for (int u = 0; u < R; ++u) {
+                        const int row = s + u * L;
+                        if (row < m) {
+                            W[p * m + row] = P[u];
+                            W[q * m + row] = Q[u];
+                        }
+                    }
+                    if (s == 0) { cn[p] = cp; cn[q] = cq; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    long long t1 = clock64();
+    if (tid == 0) atomicAdd((unsigned long long*)clk, (unsigned long long)(t1 - t0));
+    if (tid == 0) out[blockIdx.x] = make_double2(W[0].x + rots, mymax);
+}
+template <int MINB>
+void run16(int m, int sweeps, const char* name) {
+    const int ctas = 148 * 2 * 4;
+    double2* out; long long* clk;
+    cudaMalloc(&out, ctas * sizeof(double2)); cudaMalloc(&clk, 8);
+    const int smem = MINB == 1 ? 150 * 1024 : m * m * 16;
+    cudaFuncSetAttribute(sweep_bench16<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(clk, 0, 8);
+        cudaEventRecord(a);
+        sweep_bench16<MINB><<<ctas, 512, smem>>>(out, m, sweeps, clk);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        const double rounds = (double)sweeps * (m - 1);
+        printf("%-12s %.3f ms  SM-cycles/round-of-one-bin %.0f (%s)\n", name, ms,
+               ms * 1e-3 * 1.965e9 * 148 / (ctas * rounds), cudaGetErrorString(cudaGetLastError()));
+    }
+}
 int main() {
+#ifdef SB_L16
+    run16<1>(60, 4, "L16x1");
+    run16<2>(60, 4, "L16x2");
+    return 0;
+#endif
     const int m = 60, sweeps = 4, ctas = 148 * 2 * 4;
     double2* out; long long* clk;
     cudaMalloc(&out, ctas * sizeof(double2)); cudaMalloc(&clk, 8);
