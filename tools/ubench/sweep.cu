@@ -264,9 +264,8 @@ __global__ void __launch_bounds__(256, 2) sweep_bench(double2* out, int m, int s
 // 16-lane pair groups (4 rows per lane), 512 threads: the one-bin-per-SM
 // layout (MINB = 1, shared memory padded so only one CTA fits) against two
 // such CTAs per SM (MINB = 2, 64 registers)
-template <int MINB>
-__global__ void __launch_bounds__(512, MINB) sweep_bench16(double2* out, int m, int sweeps, long long* clk) {
-    constexpr int L = 16, R = 4;
+template <int MINB, int L = 16, int R = 4, int NT = 512>
+__global__ void __launch_bounds__(NT, MINB) sweep_bench16(double2* out, int m, int sweeps, long long* clk) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* W = reinterpret_cast<double2*>(smem_raw);
     __shared__ double cn[kMaxM];
@@ -322,18 +321,18 @@ __global__ void __launch_bounds__(512, MINB) sweep_bench16(double2* out, int m, 
     if (tid == 0) atomicAdd((unsigned long long*)clk, (unsigned long long)(t1 - t0));
     if (tid == 0) out[blockIdx.x] = make_double2(W[0].x + rots, mymax);
 }
-template <int MINB>
-void run16(int m, int sweeps, const char* name) {
+template <int MINB, int L = 16, int R = 4, int NT = 512>
+void run16(int m, int sweeps, const char* name, int smem_force = 0) {
     const int ctas = 148 * 2 * 4;
     double2* out; long long* clk;
     cudaMalloc(&out, ctas * sizeof(double2)); cudaMalloc(&clk, 8);
-    const int smem = MINB == 1 ? 150 * 1024 : m * m * 16;
-    cudaFuncSetAttribute(sweep_bench16<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = smem_force ? smem_force : (MINB == 1 ? 150 * 1024 : m * m * 16);
+    cudaFuncSetAttribute(sweep_bench16<MINB, L, R, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     for (int rep = 0; rep < 3; ++rep) {
         cudaMemset(clk, 0, 8);
         cudaEventRecord(a);
-        sweep_bench16<MINB><<<ctas, 512, smem>>>(out, m, sweeps, clk);
+        sweep_bench16<MINB, L, R, NT><<<ctas, NT, smem>>>(out, m, sweeps, clk);
         cudaEventRecord(b); cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         const double rounds = (double)sweeps * (m - 1);
@@ -345,6 +344,14 @@ int main() {
 #ifdef SB_L16
     run16<1>(60, 4, "L16x1");
     run16<2>(60, 4, "L16x2");
+    return 0;
+#endif
+#ifdef SB_L4
+    // 4-lane groups, 16 rows per lane, 128 threads: 2 CTAs per SM (the
+    // production scratch would allow no more) and 3
+    run16<2, 4, 16, 128>(60, 4, "L4x2", 100 * 1024);
+    run16<3, 4, 16, 128>(60, 4, "L4x3", 70 * 1024);
+    run16<2, 8, 8, 256>(60, 4, "L8x2(base)", 100 * 1024);
     return 0;
 #endif
     const int m = 60, sweeps = 4, ctas = 148 * 2 * 4;
