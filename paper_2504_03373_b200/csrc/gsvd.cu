@@ -92,15 +92,18 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
     if (t == 0) cs.collapsed = 0;  // published by the first barrier below
     // squared norms of the D columns (four lanes per column, nd <= 64)
     auto dnorms = [&](double* out) {
-        const int b = t >> 2, part = t & 3;
-        double v = 0;
-        if (b < nd) {
-            const double2* wd = W + cs.dropped[b] * m;
-            for (int i = part; i < m; i += 4) v = fma(wd[i].x, wd[i].x, fma(wd[i].y, wd[i].y, v));
+        const int part = t & 3;
+        for (int b0 = 0; b0 < nd; b0 += nt / 4) {
+            const int b = b0 + (t >> 2);
+            double v = 0;
+            if (b < nd) {
+                const double2* wd = W + cs.dropped[b] * m;
+                for (int i = part; i < m; i += 4) v = fma(wd[i].x, wd[i].x, fma(wd[i].y, wd[i].y, v));
+            }
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            if (b < nd && part == 0) out[b] = v;
         }
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        if (b < nd && part == 0) out[b] = v;
     };
     dnorms(cs.invd);
     for (int pass = 0; pass < 2; ++pass) {
@@ -232,9 +235,9 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
         if (cs.collapsed) return;  // uniform: written before the barrier above
         // row solve q_rb = (d_rb - sum_{a<b} q_ra conj(L_ba)) / L_bb, four lanes per row
         {
-            const int r = t >> 2, part = t & 3;
+            const int part = t & 3;
             const unsigned gm = 0xfu << ((t & 31) & ~3);
-            if (r < m) {
+            for (int r = t >> 2; r < m; r += nt / 4) {
                 for (int b = 0; b < nd; ++b) {
                     double2 acc = make_double2(0, 0);
                     const double2* lb = G + b * (b + 1) / 2;
@@ -589,7 +592,7 @@ __device__ void seq_vanish(double2* W, const int* perm, int m_rt, int z, double2
 
 // New columns of one group from a Z slice: W[:, cols[s]] <- sum_k W[:, cols[k]] Z[k][s]
 template <int MC>
-__device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const double2* Z) {
+__device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const double2* Z, int zld = 0) {
     const int m = MC > 0 ? MC : m_rt;
     constexpr int nt = jac_threads<MC>();
     constexpr int kOut = ((MC > 0 ? MC : kMaxM) * kZMax + nt - 1) / nt;
@@ -602,7 +605,7 @@ __device__ void apply_span_z(double2* W, int m_rt, int d, const int* cols, const
             const int i = e % m, sv = e / m;
             double2 acc = make_double2(0, 0);
             for (int k = 0; k < d; ++k) {
-                const double2 a = W[cols[k] * m + i], b = Z[k * d + sv];
+                const double2 a = W[cols[k] * m + i], b = Z[k * (zld ? zld : d) + sv];
                 acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
                 acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
             }
@@ -702,25 +705,9 @@ __device__ void pick_in_span(const double2* W, double2* Y, int m, int d, bool un
 }
 
 // W[:, cols[s]] <- sum_k W[:, cols[k]] z[k][s]  (new vectors of one group)
-template <class CS>
+template <int MC, class CS>
 __device__ void apply_span(double2* W, int m, int d, CS& cs) {
-    const int t = threadIdx.x;
-    double2 out[6];
-    int cnt = 0;
-    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) {
-        const int i = e % m, s = e / m;
-        double2 acc = make_double2(0, 0);
-        for (int k = 0; k < d; ++k) {
-            const double2 a = W[cs.cols[k] * m + i], b = cs.z[k][s];
-            acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-            acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
-        }
-        out[cnt] = acc;
-    }
-    __syncthreads();
-    cnt = 0;
-    for (int e = t; e < m * d && cnt < 6; e += blockDim.x, ++cnt) W[cs.cols[e / m] * m + (e % m)] = out[cnt];
-    __syncthreads();
+    apply_span_z<MC>(W, m, d, cs.cols, &cs.z[0][0], (int)(sizeof(cs.z[0]) / sizeof(double2)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1439,7 +1426,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
             if (tid < d) cs.cols[tid] = s_perm[i0 + tid];
             __syncthreads();
             pick_in_span(W, Y, m, d, z > 0 && gi == 0, cs);
-            apply_span(W, m, d, cs);
+            apply_span<MC>(W, m, d, cs);
         }
         // phase rule (gsvd.cpp:545-564): warp per vector
         const int warp = tid / kWarp, lane = tid % kWarp;

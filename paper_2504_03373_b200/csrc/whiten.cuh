@@ -114,17 +114,18 @@ __device__ __forceinline__ void form_whitened_staged(const float2* __restrict__ 
             stage[e] = f2d(rb[k * m + j0 + jj]);
         }
         __syncthreads();
-        if (active && nj > 0) {
+        // 8 columns per thread and pass (one pass at 256 threads, m <= 64)
+        for (int jb = 0; active && jb < nj; jb += 8 * parts) {
             double2 acc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) acc[u] = make_double2(0, 0);
             whiten_rows(krow, stage, m, nj, acc, [&](int u) {
-                const int jj = part + u * parts;
+                const int jj = jb + part + u * parts;
                 return jj < nj ? jj : -1;
             });
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int jj = part + u * parts;
+                const int jj = jb + part + u * parts;
                 if (jj < nj) W[(j0 + jj) * m + i] = acc[u];
             }
         }
