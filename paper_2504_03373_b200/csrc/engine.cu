@@ -105,6 +105,8 @@ struct sslg_ctx {
     uint8_t* conv = nullptr;
     uint32_t* work = nullptr;  // generic-canonicalization worklist
     double2* ascratch = nullptr;  // A copies for the preconditioned back-multiply
+    double2* wscratch = nullptr;  // W between the split solver kernels (m = 60)
+    int* pivs = nullptr;          // QR pivots between them
     long long* phase_clk = nullptr;  // solver phase clocks (SSLG_PHASE_CLOCKS=1)
     double* p = nullptr;
     double* power = nullptr;
@@ -197,8 +199,9 @@ int run_gsvd(sslg_ctx* c, int n) {
                 g.max_sweeps ? (int)g.max_sweeps : 60, g.canonical_subspaces, g.refine_leading,
                 g.precondition, c->ascratch, c->phase_clk};
     ga.abort = c->abort;
-    launch_jacobi(ga, n, c->stream);
-    ++c->launches;
+    ga.wscratch = c->wscratch;
+    ga.pivs = c->pivs;
+    c->launches += launch_jacobi(ga, n, c->stream);
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
     if (g.canonical_subspaces) {
@@ -382,6 +385,10 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     rc |= dalloc(&c->conv, NB * B);
     rc |= dalloc(&c->work, NB * B + 2);
     if (g.precondition) rc |= dalloc(&c->ascratch, NB * B * mm);
+    if (g.precondition && g.m == 60 && !std::getenv("SSLG_FUSED_SOLVER")) {
+        rc |= dalloc(&c->wscratch, NB * B * mm);
+        rc |= dalloc(&c->pivs, NB * B * 64);
+    }
     if (const char* pc = std::getenv("SSLG_PHASE_CLOCKS"); pc && pc[0] == '1') {
         rc |= dalloc(&c->phase_clk, 8);
         if (!rc) cudaMemset(c->phase_clk, 0, 8 * sizeof(long long));
@@ -418,7 +425,7 @@ void sslg_destroy(sslg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->k,      c->kinv,  c->h_raw, c->h_t,   c->num,     c->nbr_off, c->nbr,
                     c->ring,   c->state, c->r,     c->sigma, c->e,       c->e_tmp,   c->sweeps,
-                    c->conv,   c->work, c->ascratch, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    c->conv,   c->work, c->ascratch, c->wscratch, c->pivs, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
                     c->flags};
     for (void* p : ptrs)
         if (p) cudaFree(p);

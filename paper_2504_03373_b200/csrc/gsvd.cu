@@ -1083,55 +1083,19 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
     return !__syncthreads_or(bad);
 }
 
-// resident CTAs per SM: 2 for the 60/64-channel solver (shared memory), 12 at
-// m = 8 and 8 at m = 16 (registers; measured best: C1 0.44 -> 0.36 ms,
-// C2 1.03 -> 0.93 ms per 32 blocks against 6)
-template <int MC>
-constexpr int jac_ctas() { return MC > 0 && MC <= 8 ? 12 : (MC > 0 && MC <= 16 ? 8 : 2); }
-
-// MC > 0: channel count fixed at compile time (loop bounds, predicates and
-// addressing fold away); MC == 0: any m <= 64 at run time.
-template <int MC>
-__global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kernel(GsvdArgs a) {
-    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int m = MC > 0 ? MC : a.m;
-    double2* W = reinterpret_cast<double2*>(smem_raw);  // [m cols][m rows]
-    double2* Y = W + m * m;                             // [kMaxM][kYld] picker coordinates
-    __shared__ double cn[kMaxM];
-    __shared__ double s_drop;
-    __shared__ int s_perm[kMaxM];  // rank -> column
-    __shared__ double s_sig[kMaxM];
-    __shared__ CanonScratchFor<MC> cs;
-    __shared__ QrScratch qs;
-
-    const int blk = blockIdx.x;
-    const int bin = blk % a.bins;
+// The one-sided Jacobi sweeps (gsvd.cpp:622-695) on W in shared memory with
+// LPP-lane pair groups (RW = 64 / LPP rows per lane); shared by the fused
+// solver (LPP = 8) and the split sweep kernel (LPP = 4, 128 threads).
+// Returns the sweep count and convergence; drop_out is the last sweep's
+// drop line (the non-preconditioned path marks columns below it).
+template <int MC, int LPP>
+__device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const GsvdArgs& a, int& sweep_out,
+                           bool& conv_out, double& drop_out) {
+    constexpr int RW = kMaxM / LPP;
     const int tid = threadIdx.x;
-
-    // optional phase clocks (SSLG_PHASE_CLOCKS): whiten, QR, sweeps, sigma /
-    // back-multiply, canonicalization, store
-    long long clk0 = 0;
-    auto mark = [&](int ph) {
-        if (a.phase_clk && tid == 0) {
-            const long long now = clock64();
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk + ph), (unsigned long long)(now - clk0));
-            clk0 = now;
-        }
-    };
-    if (tid == 0) clk0 = clock64();
-    form_whitened_staged(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W, Y);
-    mark(0);
-    const bool precond = a.precondition && a.ascratch;
-    double2* ag = precond ? a.ascratch + (size_t)blk * m * m : nullptr;
-    if (precond) {
-        for (int e = tid; e < m * m; e += blockDim.x) ag[e] = W[e];
-        qrcp_to_rh<MC>(W, m, qs);
-    }
-    mark(1);
-
-    const int g = tid / kLPP;
-    const int s = tid % kLPP;
+    __shared__ double s_drop;
+    const int g = tid / LPP;
+    const int s = tid % LPP;
     const int n_even = (m + 1) & ~1;
     const int npairs = n_even / 2;
 
@@ -1154,14 +1118,14 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
             if (j < m) {
                 double v = 0;
 #pragma unroll
-                for (int u = 0; u < kRows; ++u) {
-                    const int row = s + u * kLPP;
+                for (int u = 0; u < RW; ++u) {
+                    const int row = s + u * LPP;
                     if (row < m) {
                         const double2 w = W[j * m + row];
                         v = fma(w.x, w.x, fma(w.y, w.y, v));
                     }
                 }
-                v = group_sum<kLPP>(v);
+                v = group_sum<LPP>(v);
                 if (s == 0) cn[j] = v;
             }
         }
@@ -1195,24 +1159,24 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
         double mymax = 0.0;
         bool rot = false;
         // round-robin (circle) ordering: the m/2 disjoint pairs of a round
-        // rotate concurrently, one kLPP-lane group per pair
+        // rotate concurrently, one LPP-lane group per pair
         for (int r = 0; r < n_even - 1; ++r) {
             if (g < npairs) {
                 int p, q;
                 rr_pair(r, g, n_even, p, q);
                 if (q < m) {
-                    double2 P[kRows], Q[kRows];
+                    double2 P[RW], Q[RW];
 #pragma unroll
-                    for (int u = 0; u < kRows; ++u) {
-                        const int row = s + u * kLPP;
+                    for (int u = 0; u < RW; ++u) {
+                        const int row = s + u * LPP;
                         P[u] = row < m ? W[p * m + row] : make_double2(0, 0);
                         Q[u] = row < m ? W[q * m + row] : make_double2(0, 0);
                     }
                     double cp = cn[p], cq = cn[q];
-                    if (rotate_pair<kRows, kLPP>(P, Q, cp, cq, drop, s, m, mymax)) {
+                    if (rotate_pair<RW, LPP>(P, Q, cp, cq, drop, s, m, mymax)) {
 #pragma unroll
-                        for (int u = 0; u < kRows; ++u) {
-                            const int row = s + u * kLPP;
+                        for (int u = 0; u < RW; ++u) {
+                            const int row = s + u * LPP;
                             if (row < m) {
                                 W[p * m + row] = P[u];
                                 W[q * m + row] = Q[u];
@@ -1245,6 +1209,81 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
         prev_maxrel = s_maxrel ? 1.0 : 0.0;
     }
 
+    sweep_out = sweep;
+    conv_out = converged;
+    drop_out = s_drop;
+}
+
+// resident CTAs per SM: 2 for the 60/64-channel solver (shared memory), 12 at
+// m = 8 and 8 at m = 16 (registers; measured best: C1 0.44 -> 0.36 ms,
+// C2 1.03 -> 0.93 ms per 32 blocks against 6)
+template <int MC>
+constexpr int jac_ctas() { return MC > 0 && MC <= 8 ? 12 : (MC > 0 && MC <= 16 ? 8 : 2); }
+
+// MC > 0: channel count fixed at compile time (loop bounds, predicates and
+// addressing fold away); MC == 0: any m <= 64 at run time.
+// PART 0: the whole solve; 1: whitening + QR, W and the pivots to global;
+// 3: the rest, after sweep_kernel ran the sweeps on the stored W.
+template <int MC, int PART = 0>
+__global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kernel(GsvdArgs a) {
+    if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = MC > 0 ? MC : a.m;
+    double2* W = reinterpret_cast<double2*>(smem_raw);  // [m cols][m rows]
+    double2* Y = W + m * m;                             // [kMaxM][kYld] picker coordinates
+    __shared__ double cn[kMaxM];
+    __shared__ int s_perm[kMaxM];  // rank -> column
+    __shared__ double s_sig[kMaxM];
+    __shared__ CanonScratchFor<MC> cs;
+    __shared__ QrScratch qs;
+
+    const int blk = blockIdx.x;
+    const int bin = blk % a.bins;
+    const int tid = threadIdx.x;
+
+    // optional phase clocks (SSLG_PHASE_CLOCKS): whiten, QR, sweeps, sigma /
+    // back-multiply, canonicalization, store
+    long long clk0 = 0;
+    auto mark = [&](int ph) {
+        if (a.phase_clk && tid == 0) {
+            const long long now = clock64();
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk + ph), (unsigned long long)(now - clk0));
+            clk0 = now;
+        }
+    };
+    if (tid == 0) clk0 = clock64();
+    const bool precond = a.precondition && a.ascratch;
+    double2* ag = precond ? a.ascratch + (size_t)blk * m * m : nullptr;
+    int sweep = 0;
+    bool converged = false;
+    double drop_last = 0.0;
+    if constexpr (PART != 3) {
+        form_whitened_staged(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W, Y);
+        mark(0);
+        if (precond) {
+            for (int e = tid; e < m * m; e += blockDim.x) ag[e] = W[e];
+            qrcp_to_rh<MC>(W, m, qs);
+        }
+        mark(1);
+    }
+    if constexpr (PART == 1) {
+        double2* wg = a.wscratch + (size_t)blk * m * m;
+        for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[e];
+        if (tid < m) a.pivs[(size_t)blk * kMaxM + tid] = qs.piv[tid];
+        return;
+    }
+    if constexpr (PART == 3) {
+        const double2* wg = a.wscratch + (size_t)blk * m * m;
+        for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
+        if (tid < m) qs.piv[tid] = a.pivs[(size_t)blk * kMaxM + tid];
+        sweep = (int)a.sweeps[blk];
+        converged = a.conv[blk] != 0;
+        __syncthreads();
+    }
+
+    if constexpr (PART == 0) run_sweeps<MC, kLPP>(W, m, cn, precond, a, sweep, converged, drop_last);
+    const int g = tid / kLPP;
+    const int s = tid % kLPP;
     mark(2);
     // sigma_j = |w_j| (gsvd.cpp:677-686), normalize in place
 #pragma unroll
@@ -1325,7 +1364,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
         int nd = 0, nc = 0;
         for (int rk = 0; rk < m; ++rk) {
             const int j = s_perm[rk];
-            const bool dropped = precond ? (rk >= r0) : !(cn[j] > s_drop);
+            const bool dropped = precond ? (rk >= r0) : !(cn[j] > drop_last);
             if (dropped) cs.dropped[nd++] = j;
             else cs.certcols[nc++] = j;
         }
@@ -1484,12 +1523,47 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     }
 }
 
-void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
+// The sweeps of the split solver: 4-lane pair groups with 16 rows per lane,
+// 128 threads and only W in shared memory, so three bins share an SM
+// (tools/ubench/sweep.cu -DSB_L4: 1471 SM-cycles per bin-round against 1638
+// for the fused 8-lane layout at two bins per SM).
+template <int MC>
+__global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
+    if (a.abort && *a.abort) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = MC;
+    double2* W = reinterpret_cast<double2*>(smem_raw);
+    __shared__ double cn[kMaxM];
+    const int blk = blockIdx.x, tid = threadIdx.x;
+    double2* wg = a.wscratch + (size_t)blk * m * m;
+    for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
+    __syncthreads();
+    int sweep = 0;
+    bool converged = false;
+    double drop = 0.0;
+    run_sweeps<MC, 4>(W, m, cn, a.precondition && a.ascratch, a, sweep, converged, drop);
+    for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[e];
+    if (tid == 0) {
+        a.sweeps[blk] = (uint32_t)sweep;
+        a.conv[blk] = converged ? 1 : 0;
+    }
+}
+
+int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
     auto launch = [&](auto kern, int threads, int mc) {
         const size_t smem = (size_t)a.m * a.m * sizeof(double2) + (size_t)scratch_entries(mc) * sizeof(double2);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<nblk * a.bins, threads, smem, s>>>(a);
     };
+    if (a.m == 60 && a.precondition && a.ascratch && a.wscratch && a.pivs) {
+        // split around the 128-thread sweep kernel
+        launch(jacobi_kernel<60, 1>, jac_threads<60>(), 60);
+        const size_t smem = (size_t)60 * 60 * sizeof(double2);
+        cudaFuncSetAttribute(sweep_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sweep_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
+        launch(jacobi_kernel<60, 3>, jac_threads<60>(), 60);
+        return 3;
+    }
     switch (a.m) {  // the BASELINE configs' channel counts get specialized code
         case 8: launch(jacobi_kernel<8>, jac_threads<8>(), 8); break;
         case 16: launch(jacobi_kernel<16>, jac_threads<16>(), 16); break;
@@ -1497,6 +1571,7 @@ void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
         case 64: launch(jacobi_kernel<64>, jac_threads<64>(), 64); break;
         default: launch(jacobi_kernel<0>, jac_threads<0>(), 0); break;
     }
+    return 1;
 }
 
 }  // namespace sslg

@@ -53,8 +53,12 @@ struct GsvdArgs {
     double2* ascratch;    // [nblk][bins][m][m] column-major copy of A (precondition)
     long long* phase_clk; // optional [8] summed SM clocks per solver phase (diagnostics)
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
+    double2* wscratch = nullptr;  // [nblk][bins][m][m] W between the split solver kernels (m = 60)
+    int* pivs = nullptr;          // [nblk][bins][64] QR column pivots between them
 };
-void launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
+// returns the number of kernels launched (1, or 3 when the solver is split
+// around a 128-thread sweep kernel)
+int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 
 struct CanonArgs {
     const float2* r;         // [nblk][bins][m][m]
