@@ -422,11 +422,17 @@ def main():
         achieved_tf = (alg["f_whiten"] + alg["f_jacobi"]) * blocks_per_launch / (jac_ms * 1e-3) / 1e12
         traffic = load_traffic()
         jac_traffic = None
-        if traffic and "jacobi_kernel" in traffic:  # ncu capture (--batch 8) scaled to this launch
+        parts = ["jacobi_prologue", "sweep_kernel", "jacobi_epilogue"]
+        if traffic and all(k in traffic for k in parts):  # ncu captures (--batch 8) scaled to this launch
+            jac_traffic = sum(traffic[k]["dram_bytes_per_launch"] / traffic[k].get("blocks_per_launch", 8)
+                              for k in parts) * blocks_per_launch
+        elif traffic and "jacobi_kernel" in traffic:
             t = traffic["jacobi_kernel"]
             jac_traffic = t["dram_bytes_per_launch"] / t.get("blocks_per_launch", 8) * blocks_per_launch
         roofline = {
-            "kernel": "jacobi_kernel (FP64 one-sided Jacobi, A = K^-1 R fused)",
+            "kernel": "GSVD solver: jacobi_kernel<60,1> (whitening A = K^-1 R + QRCP) -> sweep_kernel "
+                      "(FP64 one-sided Jacobi sweeps) -> jacobi_kernel<60,3> (sigma, back-multiply, "
+                      "canonical bases); achieved over the three launches",
             "bound": "fp64", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s",
             "frac": achieved_tf / fp64 if fp64 else None, "traffic": jac_traffic,
             "peak_kind": "measured in-run (DFMA microbenchmark, sslg_probe_fp64_tflops); "

@@ -1535,6 +1535,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
     double2* W = reinterpret_cast<double2*>(smem_raw);
     __shared__ double cn[kMaxM];
     const int blk = blockIdx.x, tid = threadIdx.x;
+    const long long clk0 = clock64();
     double2* wg = a.wscratch + (size_t)blk * m * m;
     for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
     __syncthreads();
@@ -1546,6 +1547,8 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
     if (tid == 0) {
         a.sweeps[blk] = (uint32_t)sweep;
         a.conv[blk] = converged ? 1 : 0;
+        if (a.phase_clk)  // sweeps phase (SSLG_PHASE_CLOCKS)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk + 2), (unsigned long long)(clock64() - clk0));
     }
 }
 

@@ -16,7 +16,16 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 1 --batch 8 --no-cpu-baseline --no-flush > gpurun_out/ncu_launch.log 2>&1
   echo "ncu launches rc=$?"
-  for K in ${NCU_KERNELS:-jacobi_kernel spectrum_mma_kernel correlation_kernel stft_kernel canonical_kernel}; do
+  # the split solver: per push jacobi_kernel<60,1>, sweep_kernel, jacobi_kernel<60,3>
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^jacobi_kernel" -s 2 -c 1 \
+    -o gpurun_out/prof_jacobi_prologue -f python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-flush \
+    > gpurun_out/ncu_jacobi_prologue.log 2>&1
+  echo "ncu jacobi prologue rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^jacobi_kernel" -s 3 -c 1 \
+    -o gpurun_out/prof_jacobi_epilogue -f python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-flush \
+    > gpurun_out/ncu_jacobi_epilogue.log 2>&1
+  echo "ncu jacobi epilogue rc=$?"
+  for K in ${NCU_KERNELS:-sweep_kernel spectrum_mma_kernel correlation_kernel stft_kernel canonical_kernel}; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$K" -s 1 -c 1 \
       -o gpurun_out/prof_$K -f python bench.py --steps 1 --warmup 1 --batch 8 --no-cpu-baseline --no-flush \
       > gpurun_out/ncu_$K.log 2>&1
