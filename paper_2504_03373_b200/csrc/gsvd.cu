@@ -1257,7 +1257,15 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     int sweep = 0;
     bool converged = false;
     double drop_last = 0.0;
-    if constexpr (PART != 3) {
+    if constexpr (PART == 1) {
+        // prologue of the split solver: the whitening on the FP64 tensor
+        // cores (no sweeps share this kernel's SM time), A saved on the way
+        form_whitened_mma<jac_threads<MC>()>(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W,
+                                            reinterpret_cast<float2*>(Y), ag);
+        mark(0);
+        qrcp_to_rh<MC>(W, m, qs);
+        mark(1);
+    } else if constexpr (PART == 0) {
         form_whitened_staged(a.r + (size_t)blk * m * m, a.kinv + (size_t)bin * m * m, m, W, Y);
         mark(0);
         if (precond) {

@@ -133,4 +133,76 @@ __device__ __forceinline__ void form_whitened_staged(const float2* __restrict__ 
     }
 }
 
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
+
+// A = K^-1 R on the FP64 tensor cores (DMMA m8n8k4), for the split solver's
+// prologue: K^-1 is staged in W (row-major, the A operand), R in `stage` as
+// float2 (the B operand, widened exactly at the fragment load); warp w
+// computes the 8-row strip 8w..8w+7 of A (8 complex 8x8 tiles, four real
+// MMAs per 4-wide k-step: Re += Kr Rr - Ki Ri, Im += Kr Ri + Ki Rr) in
+// registers, then writes it column-major over W and to `ag` (the saved copy
+// the back-multiplication reads).  NT threads, NT / 32 >= ceil(m / 8) warps.
+// Same products as form_whitened, summed in the tensor core's order.
+template <int NT>
+__device__ __forceinline__ void form_whitened_mma(const float2* __restrict__ rb, const double2* __restrict__ kb,
+                                                  int m, double2* W, float2* stage, double2* ag) {
+    const int t = threadIdx.x;
+    for (int e = t; e < m * m; e += NT) {
+        W[e] = kb[e];
+        stage[e] = rb[e];
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31, r = lane >> 2, c = lane & 3;
+    const int nt8 = (m + 7) >> 3;
+    double re[8][2], im[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) re[j][0] = re[j][1] = im[j][0] = im[j][1] = 0.0;
+    const int i = warp * 8 + r;
+    if (warp < nt8) {
+        for (int k0 = 0; k0 < m; k0 += 4) {
+            const int k = k0 + c;
+            const double2 av = (i < m && k < m) ? W[i * m + k] : make_double2(0, 0);
+            const double nai = -av.y;
+            double2 bv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int col = j * 8 + r;
+                bv[j] = (j < nt8 && k < m && col < m) ? f2d(stage[k * m + col]) : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nt8) {
+                    dmma_8x8x4(re[j][0], re[j][1], av.x, bv[j].x);
+                    dmma_8x8x4(im[j][0], im[j][1], av.x, bv[j].y);
+                }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nt8) {
+                    dmma_8x8x4(re[j][0], re[j][1], nai, bv[j].y);
+                    dmma_8x8x4(im[j][0], im[j][1], av.y, bv[j].x);
+                }
+        }
+    }
+    __syncthreads();  // K^-1 in W is consumed
+    if (warp < nt8) {
+        const int row = warp * 8 + r;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = j * 8 + 2 * c + e;
+                if (row < m && col < m) {
+                    const double2 v = make_double2(re[j][e], im[j][e]);
+                    W[col * m + row] = v;
+                    if (ag) ag[col * m + row] = v;
+                }
+            }
+    }
+    __syncthreads();
+}
+
 }  // namespace sslg
