@@ -1083,6 +1083,64 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
     return !__syncthreads_or(bad);
 }
 
+// U_A = A P U_X S^-1 on the FP64 tensor cores (DMMA m8n8k4) for the split
+// solver's epilogue: warp w owns output rows 8w..8w+7 (8 complex 8x8 tiles),
+// the A operand (rows of A P, column piv[k] of the saved A) comes straight
+// from global memory (L2), the B operand (U_X = normalized W) from shared
+// memory; the strip is held in registers until every warp has read W.
+template <int NT>
+__device__ void back_multiply_mma(double2* W, const double2* __restrict__ ag, int m, const QrScratch& qs,
+                                  const double* sig) {
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31, r = lane >> 2, c = lane & 3;
+    const int nt8 = (m + 7) >> 3;
+    double re[8][2], im[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) re[j][0] = re[j][1] = im[j][0] = im[j][1] = 0.0;
+    const int i = warp * 8 + r;
+    if (warp < nt8) {
+        double2 an = (i < m && c < m) ? ag[qs.piv[c] * m + i] : make_double2(0, 0);
+        for (int k0 = 0; k0 < m; k0 += 4) {
+            const int k = k0 + c;
+            const double2 av = an;  // A_P[i][k]
+            const int kn = k + 4;
+            an = (i < m && kn < m) ? ag[qs.piv[kn] * m + i] : make_double2(0, 0);  // next step's fragment
+            const double nai = -av.y;
+            double2 bv[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int col = j * 8 + r;
+                bv[j] = (j < nt8 && k < m && col < m) ? W[col * m + k] : make_double2(0, 0);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nt8) {
+                    dmma_8x8x4(re[j][0], re[j][1], av.x, bv[j].x);
+                    dmma_8x8x4(im[j][0], im[j][1], av.x, bv[j].y);
+                }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nt8) {
+                    dmma_8x8x4(re[j][0], re[j][1], nai, bv[j].y);
+                    dmma_8x8x4(im[j][0], im[j][1], av.y, bv[j].x);
+                }
+        }
+    }
+    __syncthreads();  // every warp has read U_X
+    if (warp < nt8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = j * 8 + 2 * c + e;
+                if (i < m && col < m)
+                    W[col * m + i] = sig[col] > 0 ? cscale(1.0 / sig[col], make_double2(re[j][e], im[j][e]))
+                                                  : make_double2(0, 0);
+            }
+    }
+    __syncthreads();
+}
+
 // The one-sided Jacobi sweeps (gsvd.cpp:622-695) on W in shared memory with
 // LPP-lane pair groups (RW = 64 / LPP rows per lane); shared by the fused
 // solver (LPP = 8) and the split sweep kernel (LPP = 4, 128 threads).
@@ -1328,7 +1386,10 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
         W[e] = nrm > 0 ? cscale(1.0 / nrm, W[e]) : make_double2(0, 0);
     }
     __syncthreads();
-    if (precond) back_multiply(W, ag, m, qs, s_sig);  // left vectors of X -> of A
+    if (precond) {  // left vectors of X -> of A
+        if constexpr (PART == 3) back_multiply_mma<jac_threads<MC>()>(W, ag, m, qs, s_sig);
+        else back_multiply(W, ag, m, qs, s_sig);
+    }
     mark(3);
 
     // ---- canonicalization (gsvd.cpp:470-565) ---------------------------
