@@ -78,13 +78,39 @@ struct CanonScratchT {
 template <int MC>
 using CanonScratchFor = CanonScratchT<(MC > 0 ? MC : kMaxM), (MC > 0 && MC < kZMax ? MC : kZMax)>;
 
+// C = op(A) B on the FP64 tensor cores (DMMA m8n8k4) over 8x8 complex tiles,
+// warps round-robin over the tiles; fa(i, k) and fb(k, j) return the operand
+// entries (zero outside M x K / K x N), conj(A) when CONJ; fc(i, j, v) takes
+// each result.  Used for the basis-completion projections of the split
+// solver's epilogue.
+template <bool CONJ, class FA, class FB, class FC>
+__device__ __forceinline__ void cgemm_tiles_mma(int M, int N, int K, FA fa, FB fb, FC fc) {
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, r = lane >> 2, c = lane & 3;
+    const int tm = (M + 7) >> 3, tn = (N + 7) >> 3;
+    for (int tile = warp; tile < tm * tn; tile += blockDim.x >> 5) {
+        const int i0 = (tile / tn) * 8, j0 = (tile % tn) * 8;
+        double re0 = 0, re1 = 0, im0 = 0, im1 = 0;
+        for (int k0 = 0; k0 < K; k0 += 4) {
+            const double2 av = fa(i0 + r, k0 + c);
+            const double2 bv = fb(k0 + c, j0 + r);
+            const double ai = CONJ ? -av.y : av.y;
+            dmma_8x8x4(re0, re1, av.x, bv.x);
+            dmma_8x8x4(im0, im1, av.x, bv.y);
+            dmma_8x8x4(re0, re1, -ai, bv.y);
+            dmma_8x8x4(im0, im1, ai, bv.x);
+        }
+        fc(i0 + r, j0 + 2 * c, make_double2(re0, im0));
+        fc(i0 + r, j0 + 2 * c + 1, make_double2(re1, im1));
+    }
+}
+
 // Completes the basis: the columns below the drop line (list D, rank order)
 // are orthonormalized against the certified columns C and then among
 // themselves.  Block form: D -= C (C^H D) (Gram product in the scratch G,
 // |C||D| <= m^2/4 entries), repeated only where the first pass removed more
 // than half of a column's energy, then CholeskyQR2 of D (the rank-order
 // Gram-Schmidt result).  Clears cs.eligible if a column collapses.
-template <int MC>
+template <int MC, bool MMA = false>
 __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor<MC>& cs) {
     const int m = MC > 0 ? MC : m_rt;
     const int t = threadIdx.x, nt = blockDim.x;
@@ -107,6 +133,28 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
     };
     dnorms(cs.invd);
     for (int pass = 0; pass < 2; ++pass) {
+      if constexpr (MMA) {
+        // G = C^H D and D -= C G on the tensor cores
+        cgemm_tiles_mma<true>(
+            nc, nd, m,
+            [&](int a, int k) { return (a < nc && k < m) ? W[cs.certcols[a] * m + k] : make_double2(0, 0); },
+            [&](int k, int b) { return (k < m && b < nd) ? W[cs.dropped[b] * m + k] : make_double2(0, 0); },
+            [&](int a, int b, double2 v) {
+                if (a < nc && b < nd) G[a * nd + b] = v;
+            });
+        __syncthreads();
+        cgemm_tiles_mma<false>(
+            m, nd, nc,
+            [&](int i, int a) { return (i < m && a < nc) ? W[cs.certcols[a] * m + i] : make_double2(0, 0); },
+            [&](int a, int b) { return (a < nc && b < nd) ? G[a * nd + b] : make_double2(0, 0); },
+            [&](int i, int b, double2 v) {
+                if (i < m && b < nd) {
+                    double2* w = W + cs.dropped[b] * m + i;
+                    *w = csub(*w, v);
+                }
+            });
+        __syncthreads();
+      } else {
         // G[a][b] = e_C[a]^H w_D[b], four lanes per product
         for (int e0 = 0; e0 < nc * nd; e0 += nt / 4) {
             const int e = e0 + (t >> 2), part = t & 3;
@@ -149,6 +197,7 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
             *w = csub(*w, cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])));
         }
         __syncthreads();
+      }
         if (pass == 0) {
             // "twice is enough" (Kahan): a second projection is needed only
             // where the first removed more than half of a column's energy
@@ -1447,7 +1496,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     __syncthreads();
     // the preconditioned vectors are re-orthonormalized whichever kernel
     // canonicalizes them (the generic one reads the lead vectors too)
-    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis<MC>(W, Y, m, cs);
+    if ((cs.eligible || precond) && cs.ndropped > 0) complete_basis<MC, PART == 3>(W, Y, m, cs);
     mark(4);
     bool fused = cs.eligible;
     int zf = cs.nvanish;  // the vanishing block, when the group machinery below takes it
