@@ -215,6 +215,15 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
     for (int pass = 0; pass < 2; ++pass) {
         // packed lower Gram G[i(i+1)/2 + k] = d_i^H d_k, k <= i
         const int np = nd * (nd + 1) / 2;
+        if constexpr (MMA) {
+            cgemm_tiles_mma<true>(
+                nd, nd, m,
+                [&](int i, int r) { return (i < nd && r < m) ? W[cs.dropped[i] * m + r] : make_double2(0, 0); },
+                [&](int r, int k) { return (r < m && k < nd) ? W[cs.dropped[k] * m + r] : make_double2(0, 0); },
+                [&](int i, int k, double2 v) {
+                    if (i < nd && k <= i) G[i * (i + 1) / 2 + k] = v;
+                });
+        } else
         for (int e0 = 0; e0 < np; e0 += nt / 4) {
             const int e = e0 + (t >> 2), part = t & 3;
             double2 d = make_double2(0, 0);
