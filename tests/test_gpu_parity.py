@@ -486,3 +486,28 @@ def test_tensor_core_spectrum_against_oracle(port, m, ns):
         want_p, want_bp = port.spectrum(e, h, ns, squared=squared, keep_bins=True)
         assert np.max(np.abs(got.bin_power - want_bp) / want_bp) <= 1e-9
         assert np.max(np.abs(got.power - want_p) / want_p) <= 1e-9
+
+
+@pytest.mark.parametrize("precondition", [True, False], ids=["split", "fused-plain"])
+def test_60ch_solver_paths_against_oracle(port, precondition):
+    """The 60-channel solver's two device paths on the same rank-deficient
+    pairs: the split launch sequence (QR-preconditioned: prologue, 128-thread
+    sweep kernel, epilogue) and the fused kernel on A itself (precondition
+    off), both against the oracle (gsvd_reference, gsvd.cpp:697-716)."""
+    from paper_2504_03373_b200 import ssl
+
+    m, bins = 60, 3
+    rng = np.random.default_rng(4242)
+    kb = rng.standard_normal((bins, m, m)) + 1j * rng.standard_normal((bins, m, m))
+    k = (kb @ kb.conj().transpose(0, 2, 1) / m + 0.5 * np.eye(m)).astype(np.complex64)
+    xb = rng.standard_normal((bins, m, 45)) + 1j * rng.standard_normal((bins, m, 45))
+    r = (xb @ xb.conj().transpose(0, 2, 1) / 45).astype(np.complex64)
+    eng = ssl.Engine(m, bins, window_frames=2, max_batch=2, solver=ssl.SolverConfig(precondition=precondition))
+    eng.set_noise_model(k)
+    sigma, e, _, conv = eng.gsvd(r)
+    eng.close()
+    want = port.gsvd_reference(k, r, threads=4)
+    smax = want["sigma"][:, :1]
+    assert np.all(conv)
+    assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+    assert np.max(np.abs(e[0] - want["e"])) <= 1e-6
