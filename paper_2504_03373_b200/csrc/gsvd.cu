@@ -247,7 +247,50 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
             if (e < np && (t & 3) == 0) G[e] = d;
         }
         __syncthreads();
-        if (t < kWarp) {  // right-looking Cholesky, one warp
+        if constexpr (MMA) {
+            // right-looking Cholesky over the whole CTA (the split solver's
+            // epilogue has no co-resident sweeps to hide a one-warp chain):
+            // two barriers per column, the trailing triangle flattened over
+            // every thread; per entry the same operations as the warp form
+            __syncthreads();
+            for (int j = 0; j < nd; ++j) {
+                const double gjj = G[j * (j + 1) / 2 + j].x;
+                if (!(gjj > 1e-12)) {  // projected norm <= 1e-6: collapsed (uniform)
+                    if (t == 0) {
+                        cs.eligible = 0;
+                        cs.collapsed = 1;
+                    }
+                    break;
+                }
+                const double inv = fast_rsqrt(gjj);
+                for (int i = j + 1 + t; i < nd; i += nt) {
+                    double2& gij = G[i * (i + 1) / 2 + j];
+                    gij = cscale(inv, gij);
+                }
+                if (t == 0) invd[j] = inv;
+                __syncthreads();
+                const int n = nd - j - 1;
+                for (int e = t; e < n * (n + 1) / 2; e += nt) {
+                    int ii = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+                    while (ii * (ii + 1) / 2 > e) --ii;
+                    while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+                    const int i = j + 1 + ii, k = j + 1 + (e - ii * (ii + 1) / 2);
+                    const double2 lij = G[i * (i + 1) / 2 + j], lkj = G[k * (k + 1) / 2 + j];
+                    double2& gik = G[i * (i + 1) / 2 + k];
+                    gik.x -= fma(lij.x, lkj.x, lij.y * lkj.y);
+                    gik.y -= fma(lij.y, lkj.x, -lij.x * lkj.y);
+                }
+                __syncthreads();
+            }
+            if (t == 0 && !cs.collapsed) {
+                double lo = invd[0], hi = invd[0];
+                for (int j = 1; j < nd; ++j) {
+                    lo = fmin(lo, invd[j]);
+                    hi = fmax(hi, invd[j]);
+                }
+                cs.again = hi <= 100.0 * lo ? 0 : 1;
+            }
+        } else if (t < kWarp) {  // right-looking Cholesky, one warp
             for (int j = 0; j < nd; ++j) {
                 const double gjj = G[j * (j + 1) / 2 + j].x;
                 if (!(gjj > 1e-12)) {  // projected norm <= 1e-6: collapsed
