@@ -1131,10 +1131,9 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
 // iff the next sweep would rotate nothing (gsvd.cpp:642-649).  Evaluated as
 // one 4x4-register-tiled Gram product over the upper triangle instead of a
 // full verification sweep of round-synchronized pair visits.
-template <int MC>
+template <int MC, int TS = 2>  // 2x2 tiles keep the fused kernel's register budget
 __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, double drop) {
     const int m = MC > 0 ? MC : m_rt;
-    constexpr int TS = 2;  // 2x2 tiles keep the kernel's register budget
     const int nt = (m + TS - 1) / TS;
     const int ntiles = nt * (nt + 1) / 2;
     bool bad = false;
@@ -1306,7 +1305,7 @@ __device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const Gs
         // rotation-free in 98% of bins), or only pairs coupled by <= 1e-8
         // relative, is usually rotation-free: certify that with one Gram
         // product instead of running it (7.44 -> 7.06 sweeps at C3).
-        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC>(W, m, cn, drop)) {
+        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC, LPP == 4 ? 4 : 2>(W, m, cn, drop)) {
             converged = true;
             break;
         }
