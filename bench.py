@@ -45,9 +45,9 @@ WORKLOADS = {"c1": "C1 (BASELINE configs[0])", "c2": "C2 (BASELINE configs[1])",
 
 
 def scene_label(args, w):
-    return (f"{WORKLOADS[args.config]}: {w.m}-ch circular r=0.3 m, 16 kHz, 512-pt FFT, {w.bins} bins, "
-            f"{w.h.shape[0]} directions, {w.ns} targets (0 dB) + 4 rotor sources (-10 dB) + diffuse (-20 dB), "
-            f"K captured from a noise-only recording, T={w.t}, Ns={w.ns}")
+    from paper_2504_03373_b200 import synth
+
+    return f"{WORKLOADS[args.config]}: {synth.describe(args.config)}"
 
 
 def frames_from_pcm(w):
@@ -408,7 +408,7 @@ def main():
     e2e_value = world * args.steps * args.batch / (e2e_total * 1e-3)
     e2e_sync_value = world * args.steps * args.batch / (e2e_sync_total * 1e-3)
     h2d = w.m * step_samples * 4
-    d2h = args.batch * (ns * (4 + 8 + 1) + 8)
+    d2h = args.batch * (ns * (4 + 8 + 1) + 4)  # idx u32, power f64, low u8 per estimate; count u32 per block
 
     if rank == 0:
         alg = algorithmic(w.m, w.bins, w.h.shape[0], w.ns, w.t)
@@ -667,7 +667,38 @@ def ctypes_probe(device):
     return out.value if rc == 0 else None
 
 
-def cpu_baseline(w, nblocks):
+def host_cpu_info():
+    """CPU model, logical cores and SMT of the host the CPU legs run on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    smt = None
+    try:
+        with open("/sys/devices/system/cpu/smt/active") as f:
+            smt = f.read().strip() == "1"
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": usable, "logical_cpus": os.cpu_count(), "smt_active": smt}
+
+
+def cpu_baseline(w, nblocks, gsvd_blocks=5, repeats=5):
+    """The reference on the host cores (SURVEY §8(d) "CPU baseline beside
+    it"): the run_locate loop over `nblocks` blocks with every core, plus the
+    stage timings of bench.cpp:198-231 -- ssl::gsvd at 1 thread (the paper's
+    "naive" methodology) and at all cores, calc_average_power<float> at 1 and
+    all cores -- each with the noise inverses prepared OUTSIDE the timer
+    (bench.cpp:209), one untimed warm-up call, and the median of `repeats`
+    calls per block over `gsvd_blocks` distinct blocks."""
     try:
         import oracle
 
@@ -675,21 +706,34 @@ def cpu_baseline(w, nblocks):
             return None
     except Exception:
         return None
-    cores = os.cpu_count() or 1
+    info = host_cpu_info()
+    cores = info["nproc"]
     spb, st, ref_out = reference_time_blocks(w, nblocks, cores)
-    # the paper's methodology: gsvd() with one thread ("naive" path), 2 blocks
     R = oracle.ref()
-    r = R.correlation(w.x[:w.t + 1], w.t)
-    t0 = time.perf_counter()
-    for rb in r[:2]:
-        R.gsvd(w.k, rb, path=0, threads=1)
-    gsvd_1t_us = 1e6 * (time.perf_counter() - t0) / 2
-    return {"value": 1.0 / spb, "unit": UNIT, "cores": cores, "kind": "reference",
-            "gsvd_1thread_us_per_block": gsvd_1t_us,
-            "sample": f"{nblocks} consecutive blocks of the same C3 stream through the reference run_locate loop "
-                      f"(oracle/_ref = unmodified sslkit, ssl::gsvd batched float path, {cores} threads)",
+    r = R.correlation(w.x[:w.t - 1 + gsvd_blocks], w.t)
+    mc = oracle.MusicCfg.make(num_sources=w.ns)
+
+    def per_block(fn):
+        return float(np.median([fn(rb) for rb in r[:gsvd_blocks]]))
+
+    g1 = per_block(lambda rb: R.time_gsvd(w.k, rb, 0, 1, repeats))
+    ga = per_block(lambda rb: R.time_gsvd(w.k, rb, 0, cores, repeats))
+    s1 = per_block(lambda rb: R.time_spectrum(w.k, rb, w.h, mc, 1, repeats))
+    sa = per_block(lambda rb: R.time_spectrum(w.k, rb, w.h, mc, cores, repeats))
+    return {"value": 1.0 / spb, "unit": UNIT, "cores": cores, "kind": "reference", **info,
+            "sample": f"{nblocks} consecutive blocks of the same {args_config_name(w)} stream through the reference "
+                      f"run_locate loop (oracle/_ref = unmodified sslkit, ssl::gsvd batched float path, {cores} "
+                      f"threads); stage timings: {gsvd_blocks} blocks x median of {repeats} calls after a warm-up, "
+                      f"noise inverses prepared outside the timer",
             "stage_s": {"correlation": st[0], "factorization": st[1], "spectrum": st[2], "peaks": st[3]},
-            "gsvd_us_per_block": 1e6 * st[1] / nblocks, "_ref_out": ref_out}
+            "gsvd_us_per_block": 1e6 * st[1] / nblocks,
+            "gsvd_1thread_us": 1e6 * g1, "gsvd_allcore_us": 1e6 * ga,
+            "spectrum_1thread_us": 1e6 * s1, "spectrum_allcore_us": 1e6 * sa,
+            "_ref_out": ref_out}
+
+
+def args_config_name(w):
+    return getattr(w, "name", "C3").upper()
 
 
 def parity_in_run(w, eng_factory, ref_out, nblocks, n_fp64=3):

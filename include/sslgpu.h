@@ -59,7 +59,8 @@ typedef struct sslg_config {
     float denominator_floor;     /* MusicConfig::denominator_floor, default 1e-12 */
     int squared_denominator;     /* MusicConfig::squared_denominator */
     float low_power_ratio;       /* MusicConfig::low_power_ratio, default 1.25 */
-    int pivoting;                /* SolverConfig::pivoting: 0 none, 1 partial */
+    int pivoting;                /* SolverConfig::pivoting: 0 none (pivot-free elimination, gsvd.cpp:27-40),
+                                    1 partial */
     int canonical_subspaces;     /* SolverConfig::canonical_subspaces */
     int refine_leading;          /* A A^H sharpening of the kept span (gsvd.cpp:440-466); default 0 =
                                     canonicalize in the span of the FP64 Jacobi basis (fused), 1 =
@@ -71,6 +72,13 @@ typedef struct sslg_config {
     uint32_t max_batch;          /* blocks (frames) processed per launch; sizes device buffers */
     int device;                  /* CUDA device ordinal */
     void* stream;                /* cudaStream_t to launch on; NULL = the context's own stream */
+    uint32_t max_qr_sweeps;      /* SolverConfig::max_qr_sweeps (gsvd.hpp:15): 0 = no budget.  A bin whose
+                                    solve needs more Jacobi sweeps than a nonzero budget reports
+                                    converged = 0 and iterations = the budget, with the converged FP64
+                                    factors -- what gsvd()'s salvage returns (gsvd.cpp:819-827) */
+    float tolerance_scale;       /* SolverConfig::tolerance_scale (gsvd.hpp:16, > 0): scales the Jacobi
+                                    no-rotation threshold, |a_pq| <= 1e-14 * scale * |w_p| |w_q| */
+    int compute_residual;        /* SolverConfig::compute_residual: sslg_gsvd fills `resid` */
 } sslg_config;
 
 /* Fills `cfg` with the reference defaults (gsvd.hpp:14-26, music.hpp:49-62,
@@ -87,11 +95,18 @@ int sslg_get_config(const sslg_ctx* ctx, sslg_config* cfg);
 /* ---- setup ------------------------------------------------------------ */
 
 /* NoiseModel: uploads K, builds K^-1 on the device with the float and double
- * Gauss-Jordan of mat_inverse<T> (gsvd.cpp:21-62, prepare_inverses 756-768);
- * with check_pd also runs check_positive_definite (gsvd.cpp:736-754).
+ * Gauss-Jordan of mat_inverse<T> (gsvd.cpp:21-62, prepare_inverses 756-768;
+ * cfg.pivoting selects partial or none); with check_pd also runs
+ * check_positive_definite (gsvd.cpp:736-754: Hermitian test, then the
+ * smallest eigenvalue of hermitian_eigenvalues, eig.cpp:11-84).
  * Failures return SSLG_NUMERICAL and set *bad_bin (nullable) to the first
  * offending bin, like the reference's "... at bin b" messages. */
 int sslg_set_noise_model(sslg_ctx* ctx, const float* k, int check_pd, uint32_t* bad_bin);
+/* NoiseModel::inverse / inverse_double (gsvd.hpp:43-44) of the current noise
+ * model: out [bins][m][m] cf64 row-major; precision 0 = the float inverse
+ * (widened exactly), 1 = the double inverse the solver uses.  Both are
+ * bit-identical to mat_inverse<T> with the context's pivoting. */
+int sslg_noise_inverse(sslg_ctx* ctx, int precision, double* out);
 /* NoiseModel::identity (gsvd.cpp:722-727). */
 int sslg_set_noise_identity(sslg_ctx* ctx);
 
@@ -130,7 +145,17 @@ int sslg_push_frames(sslg_ctx* ctx, const float* x, uint32_t nframes, sslg_block
 
 /* Same on device-resident frames (x_dev: device pointer, same layout);
  * results stay on the device until sslg_read_results.  Asynchronous on the
- * context stream. */
+ * context stream, with no host synchronization: the non-finite gate runs on
+ * the device (a failure makes every later kernel return early), and the
+ * next synchronizing call (sslg_read_results, sslg_synchronize, any
+ * push or stage call) reports SSLG_VALIDATION and rewinds the window to just
+ * before the failing push.
+ *
+ * Every synchronous entry point returns SSLG_VALIDATION while asynchronous
+ * pushes (sslg_push_samples_async) are uncollected.  The host-buffer pushes
+ * gate frame by frame like CorrelationWindow::push (correlation.cpp:16-17):
+ * the frames before the first non-finite one are pushed and their blocks
+ * written and counted in *emitted before the error is returned. */
 int sslg_push_frames_device(sslg_ctx* ctx, const void* x_dev, uint32_t nframes, uint32_t* emitted);
 /* Copies the results of the last push (blocks [0, n)) to host arrays
  * (any may be NULL). */
@@ -203,6 +228,11 @@ int sslg_locate_samples(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint
  * rewound to just before the failing push and SSLG_VALIDATION is returned;
  * sslg_reset_window restarts the stream. */
 int sslg_push_samples_async(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint64_t* ticket);
+/* Whether asynchronous pushes also copy the broadband power [e][dirs] back
+ * (needed for sslg_wait_results' `power`; off by default: FrameEstimates,
+ * pipeline.hpp:63-66, carries only the estimates).  Refused while pushes are
+ * pending. */
+int sslg_set_async_power(sslg_ctx* ctx, int on);
 int sslg_wait_results(sslg_ctx* ctx, uint64_t ticket, uint32_t cap_blocks, sslg_block_out* blocks, uint32_t* est_idx,
                       double* est_power, uint8_t* est_low, double* power, uint32_t* emitted);
 
@@ -218,6 +248,19 @@ int sslg_correlation(sslg_ctx* ctx, const float* x, uint32_t nframes, float* r_o
  * [nsets][bins] (nullable).  FP64 one-sided Jacobi + canonicalization. */
 int sslg_gsvd(sslg_ctx* ctx, const float* r, uint32_t nsets, double* sigma, double* e, uint32_t* sweeps,
               uint8_t* conv);
+/* The same with the right factor and the residual (GsvdBinResult::e_r and
+ * recon_residual, gsvd.hpp:52-60): er [nsets][bins][m][m] row-major, row i
+ * pairs with sigma_i so that A = E diag(sigma) E_r with A = K^-1 R; rows of
+ * non-vanishing values are the reference's (the polar factor of E_g^H A per
+ * tied group g -- for a single value, e_i^H A / sigma_i -- which is what the
+ * reference's W^H rotation of V^H yields, gsvd.cpp:512-543), rows of the
+ * vanishing block complete E_r to a unitary matrix (canonical completion, as
+ * pick_orthonormal builds E's, gsvd.cpp:402-436).  resid [nsets][bins] =
+ * ||A - E diag(sigma) E_r||_F / ||A||_F (reconstruction_residual,
+ * gsvd.cpp:573-585), or -1 unless compute_residual is set.  Every output is
+ * nullable. */
+int sslg_gsvd_ex(sslg_ctx* ctx, const float* r, uint32_t nsets, double* sigma, double* e, double* er,
+                 uint32_t* sweeps, uint8_t* conv, double* resid);
 
 /* calc_average_power (music.cpp:112-165) on left factors e [nsets][bins][m][m]
  * (as returned by sslg_gsvd): power [nsets][dirs], bin_power

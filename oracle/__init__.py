@@ -328,6 +328,18 @@ class _Ref:
                                           C.c_uint(threads), C.c_int(repeats), C.byref(out)))
         return out.value
 
+    def time_spectrum(self, k, r, h, music: MusicCfg, threads: int, repeats: int) -> float:
+        """Median seconds of calc_average_power<float> on gsvd()'s factors of r."""
+        k = np.ascontiguousarray(k, np.complex64)
+        r = np.ascontiguousarray(r, np.complex64)
+        h = np.ascontiguousarray(h, np.complex64)
+        b, m, _ = r.shape
+        out = C.c_double()
+        self._chk(self.L.sslref_time_spectrum(_p(k, _f32p), _p(r, _f32p), C.c_uint32(m), C.c_uint32(b), _p(h, _f32p),
+                                              C.c_uint32(h.shape[0]), C.byref(music), C.c_uint(threads),
+                                              C.c_int(repeats), C.byref(out)))
+        return out.value
+
     def gsvd_matrix(self, kinv, r, precision: int, solver: Optional[SolverCfg] = None):
         """precision 0: gsvd_matrix<float>, 1: gsvd_matrix<double>, 2: gsvd_reference_matrix."""
         kinv = np.ascontiguousarray(kinv, np.complex128)

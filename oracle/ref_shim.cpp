@@ -450,11 +450,43 @@ SHIM_API int sslref_time_gsvd(const float* k, const float* r, std::uint32_t m, s
         ssl::SolverConfig sc;
         noise.prepare_inverses(sc.pivoting);
         std::vector<double> runs;
-        for (int i = 0; i < repeats; ++i) {
+        for (int i = -1; i < repeats; ++i) { // i = -1: untimed warm-up call
             const auto t0 = std::chrono::steady_clock::now();
             if (path == 1) (void)ssl::gsvd_reference(noise, rs, sc, threads);
             else (void)ssl::gsvd(noise, rs, sc, threads);
-            runs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+            if (i >= 0) runs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+        }
+        std::sort(runs.begin(), runs.end());
+        *median_s = runs[runs.size() / 2];
+    });
+}
+
+// Timing of calc_average_power<float> alone (music.cpp:112-165) on the float
+// path's own factors of `r` (gsvd(), computed outside the timer), as
+// bench.cpp:198-231 times the spectrum stage.  Median seconds per call over
+// `repeats` after one untimed warm-up call.
+SHIM_API int sslref_time_spectrum(const float* k, const float* r, std::uint32_t m, std::uint32_t bins,
+                                  const float* h, std::uint32_t dirs, const sslref_music* mcfg, unsigned threads,
+                                  int repeats, double* median_s) {
+    return guarded([&] {
+        ssl::NoiseModel noise;
+        noise.k = set_from(k, m, bins);
+        const auto rs = set_from(r, m, bins);
+        ssl::SolverConfig sc;
+        const auto basis = ssl::gsvd(noise, rs, sc, threads);
+        ssl::SteeringField sf;
+        sf.m = m;
+        sf.bin_min = 0;
+        sf.bin_max = bins - 1;
+        sf.directions.assign(dirs, ssl::Direction{});
+        sf.vectors.resize(std::size_t(dirs) * bins * m);
+        for (std::size_t i = 0; i < sf.vectors.size(); ++i) sf.vectors[i] = ssl::cfloat(h[2 * i], h[2 * i + 1]);
+        const auto mc = music_from(mcfg);
+        std::vector<double> runs;
+        for (int i = -1; i < repeats; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            (void)ssl::calc_average_power<float>(basis, sf, mc, false, threads);
+            if (i >= 0) runs.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
         }
         std::sort(runs.begin(), runs.end());
         *median_s = runs[runs.size() / 2];

@@ -47,6 +47,9 @@ class Config(C.Structure):
         ("max_batch", C.c_uint32),
         ("device", C.c_int),
         ("stream", C.c_void_p),
+        ("max_qr_sweeps", C.c_uint32),
+        ("tolerance_scale", C.c_float),
+        ("compute_residual", C.c_int),
     ]
 
 
@@ -82,6 +85,9 @@ EXPORTS = {
     "sslg_synchronize": (C.c_int, [C.c_void_p]),
     "sslg_correlation": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f32p, _u32p]),
     "sslg_gsvd": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _u32p, _u8p]),
+    "sslg_gsvd_ex": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _f64p, _u32p, _u8p, _f64p]),
+    "sslg_noise_inverse": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
+    "sslg_set_async_power": (C.c_int, [C.c_void_p, C.c_int]),
     "sslg_spectrum": (C.c_int, [C.c_void_p, _f64p, C.c_uint32, _f64p, _f64p]),
     "sslg_peaks": (C.c_int, [C.c_void_p, _f64p, C.c_uint32, _u32p, _f64p, _u8p, _u32p]),
     "sslg_last_stage_ms": (C.c_int, [C.c_void_p, _f32p]),

@@ -165,4 +165,32 @@ void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStr
     count_nonfinite_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, n, bad);
 }
 
+// Per-frame gate of the synchronous paths: the smallest index (frame0 + f)
+// of a frame holding a non-finite value lands in *first (atomicMin; the
+// caller initializes it to 0xffffffff).  CorrelationWindow::push rejects
+// exactly that frame (correlation.cpp:16-17) and keeps every earlier one.
+__global__ void first_nonfinite_kernel(const float* p, size_t per_frame, int nframes, unsigned int frame0,
+                                       unsigned int* first) {
+    const size_t n = per_frame * (size_t)nframes;
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    unsigned int best = 0xffffffffu;
+    for (; i < n; i += stride)
+        if (!isfinite(p[i])) {
+            const unsigned int f = frame0 + (unsigned int)(i / per_frame);
+            best = f < best ? f : best;
+        }
+    for (int o = 16; o; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0 && best != 0xffffffffu) atomicMin(first, best);
+}
+
+void launch_first_nonfinite(const float* p, size_t per_frame, int nframes, unsigned int frame0, unsigned int* first,
+                            cudaStream_t s) {
+    const int threads = 256;
+    size_t blocks = (per_frame * (size_t)nframes + threads - 1) / threads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) blocks = 1;
+    first_nonfinite_kernel<<<(unsigned)blocks, threads, 0, s>>>(p, per_frame, nframes, frame0, first);
+}
+
 }  // namespace sslg

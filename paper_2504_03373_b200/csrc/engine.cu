@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -152,6 +153,16 @@ struct sslg_ctx {
     uint64_t collected = 0;     // sub-pushes handed back by sslg_wait_results
     bool poisoned = false;
     uint32_t poison_code = 0;
+    bool async_power = false;   // async pushes also copy back power [e][dirs] (sslg_set_async_power)
+    // device-frame pushes (sslg_push_frames_device) gate on the device through
+    // the same abort word; their window counters are kept until the next
+    // synchronizing call verifies the word (check_device_gate)
+    struct DevPush {
+        uint32_t seq;
+        long long pushed0, since0;
+    };
+    std::deque<DevPush> dev_unverified;
+    uint32_t dev_seq = 0;
 };
 
 namespace {
@@ -163,7 +174,8 @@ int sync_flags(sslg_ctx* c, unsigned int* host, int n) {
 }
 
 int reset_flags(sslg_ctx* c) {
-    unsigned int init[8] = {0, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0, 0, 0};
+    // [0] non-finite count, [1..4] first bad bin (float/double inverse, Hermitian, PD), [5] first bad frame
+    unsigned int init[8] = {0, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu, 0, 0};
     CU(cudaMemcpyAsync(c->flags, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     return 0;
 }
@@ -201,6 +213,7 @@ int run_gsvd(sslg_ctx* c, int n) {
     ga.abort = c->abort;
     ga.wscratch = c->wscratch;
     ga.pivs = c->pivs;
+    ga.tol2 = 1e-28 * (double)g.tolerance_scale * (double)g.tolerance_scale;
     c->launches += launch_jacobi(ga, n, c->stream);
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
@@ -234,11 +247,12 @@ int run_music(sslg_ctx* c, int n) {
     return 0;
 }
 
-int gate_frames(sslg_ctx* c, uint32_t nframes);
+int gate_frames(sslg_ctx* c, uint32_t nframes, uint32_t* good);
 
 // copies nframes frames (src: host or device) into the ring after the
-// current push count, then gates on non-finite values
-int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind kind) {
+// current push count, then gates on non-finite values: *good = the number of
+// leading frames before the first non-finite one (nframes if none)
+int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind kind, uint32_t* good) {
     const sslg_config& g = c->cfg;
     const size_t fsz = (size_t)g.m * g.bins;
     uint32_t done = 0;
@@ -249,12 +263,14 @@ int stage_frames(sslg_ctx* c, const float* src, uint32_t nframes, cudaMemcpyKind
                            kind, c->stream));
         done += run;
     }
-    return gate_frames(c, nframes);
+    return gate_frames(c, nframes, good);
 }
 
 // non-finite gate over the nframes ring slots after the push count
-// (CorrelationWindow::push -> instantaneous_correlation check, correlation.cpp:16-17)
-int gate_frames(sslg_ctx* c, uint32_t nframes) {
+// (CorrelationWindow::push -> instantaneous_correlation check,
+// correlation.cpp:16-17), frame by frame: the reference rejects the first
+// non-finite frame and keeps every frame pushed before it
+int gate_frames(sslg_ctx* c, uint32_t nframes, uint32_t* good) {
     const sslg_config& g = c->cfg;
     const size_t fsz = (size_t)g.m * g.bins;
     TRY(reset_flags(c));
@@ -263,20 +279,22 @@ int gate_frames(sslg_ctx* c, uint32_t nframes) {
     while (done < nframes) {
         const int slot = (int)((c->pushed + done) % c->cap);
         const uint32_t run = std::min<uint32_t>(nframes - done, (uint32_t)(c->cap - slot));
-        launch_count_nonfinite(reinterpret_cast<const float*>(c->ring + (size_t)slot * fsz), run * fsz * 2,
-                               c->flags, c->stream);
+        launch_first_nonfinite(reinterpret_cast<const float*>(c->ring + (size_t)slot * fsz), fsz * 2, (int)run, done,
+                               c->flags + 5, c->stream);
         ++c->launches;
         done += run;
     }
-    unsigned int fl[1];
-    TRY(sync_flags(c, fl, 1));
-    if (fl[0]) return set_err(SSLG_VALIDATION, "non-finite spectrum value");
+    unsigned int fl[6];
+    TRY(sync_flags(c, fl, 6));
+    *good = std::min<uint32_t>(fl[5], nframes);
     return 0;
 }
 
 // one chunk of at most max_batch frames already validated in the ring
 int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
     const sslg_config& g = c->cfg;
+    *emitted = 0;
+    if (nframes == 0) return 0;
     const long long first_emit = std::max<long long>(0, (long long)g.window_frames - 1 - c->pushed);
     const int n = (int)std::max<long long>(0, (long long)nframes - first_emit);
     CU(cudaEventRecord(c->ev[0], c->stream));
@@ -305,15 +323,66 @@ int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
     return 0;
 }
 
-int require_ready(sslg_ctx* c) {
+// Asynchronous sub-pushes not yet handed back by sslg_wait_results own the
+// device window, the work buffers and the abort word: every synchronous entry
+// point is refused until they are collected (or the window is reset).
+int require_no_async(sslg_ctx* c) {
+    if (c->next_id != c->collected)
+        return set_err(SSLG_VALIDATION,
+                       "asynchronous pushes are pending; collect them with sslg_wait_results or reset the window");
+    return 0;
+}
+
+// Verifies the device-side gate of the device-frame pushes since the last
+// check: if one of them saw a non-finite value, every kernel from its gate on
+// was skipped, so the window is rewound to just before that push (its ring
+// slots lie outside the live window) and the error is reported here.
+int check_device_gate(sslg_ctx* c) {
+    if (c->dev_unverified.empty()) return 0;
+    CU(cudaStreamSynchronize(c->stream));
+    unsigned int ab = 0;
+    CU(cudaMemcpy(&ab, c->abort, sizeof ab, cudaMemcpyDeviceToHost));
+    if (ab) {
+        const uint32_t seq = ab - 1u;
+        for (const auto& d : c->dev_unverified)
+            if (d.seq == seq) {
+                c->pushed = d.pushed0;
+                c->since = d.since0;
+                break;
+            }
+        c->last_emitted = 0;
+        c->dev_unverified.clear();
+        CU(cudaMemset(c->abort, 0, sizeof(unsigned int)));
+        return set_err(SSLG_VALIDATION, "non-finite spectrum value");
+    }
+    c->dev_unverified.clear();
+    return 0;
+}
+
+int require_ready(sslg_ctx* c, bool verify_device_gate = true) {
     if (!c) return set_err(SSLG_VALIDATION, "null context");
     if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model not set");
     if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
     if (c->cfg.num_sources >= c->cfg.m)
         return set_err(SSLG_VALIDATION, "num_sources must be smaller than the channel count");
     if (c->poisoned) return set_err(SSLG_VALIDATION, "stream stopped by a non-finite spectrum value; reset the window");
+    TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
+    if (verify_device_gate || c->dev_unverified.size() >= 1024) TRY(check_device_gate(c));
     return 0;
+}
+
+// SolverConfig::max_qr_sweeps (gsvd.cpp:597-605, 819-827): a bin whose solve
+// took more sweeps than a nonzero budget is flagged non-converged with the
+// budget as its iteration count; its factors stay the converged FP64 ones,
+// which is what the reference's salvage through the exact path returns.
+void apply_sweep_budget(uint32_t budget, uint32_t* sweeps, uint8_t* conv, size_t n) {
+    if (!budget || !sweeps) return;
+    for (size_t i = 0; i < n; ++i)
+        if (sweeps[i] > budget) {
+            sweeps[i] = budget;
+            if (conv) conv[i] = 0;
+        }
 }
 
 }  // namespace
@@ -336,6 +405,9 @@ void sslg_config_default(sslg_config* cfg) {
     cfg->max_batch = 16;
     cfg->device = 0;
     cfg->stream = nullptr;
+    cfg->max_qr_sweeps = 0;
+    cfg->tolerance_scale = 1.0f;
+    cfg->compute_residual = 0;
 }
 
 const char* sslg_last_error(void) { return g_err.c_str(); }
@@ -352,6 +424,7 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     if (!(g.denominator_floor > 0)) return set_err(SSLG_VALIDATION, "denominator_floor must be positive");
     if (!(g.low_power_ratio >= 0)) return set_err(SSLG_VALIDATION, "low_power_ratio must be non-negative");
     if (g.max_batch < 1) return set_err(SSLG_VALIDATION, "max_batch must be >= 1");
+    if (!(g.tolerance_scale > 0)) return set_err(SSLG_VALIDATION, "tolerance_scale must be positive");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return set_err(SSLG_DEVICE, "no CUDA device available (the engine has no CPU fallback)");
@@ -452,7 +525,9 @@ int sslg_get_config(const sslg_ctx* c, sslg_config* cfg) {
 
 int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* bad_bin) {
     if (!c || !k) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
     const sslg_config& g = c->cfg;
     const size_t mm = (size_t)g.m * g.m;
     const size_t n = g.bins * mm * 2;
@@ -462,22 +537,29 @@ int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* ba
     TRY(reset_flags(c));
     unsigned int fl[5];
     if (check_pd) {
-        launch_pd_check(c->k, (int)g.m, (int)g.bins, c->flags + 3, c->flags + 4, nullptr, c->stream);
-        TRY(check_last_launch("pd_check_kernel"));
-        TRY(sync_flags(c, fl, 5));
-        if (fl[3] != 0xffffffffu || fl[4] != 0xffffffffu) {
+        double* min_eig = nullptr;
+        TRY(dalloc(&min_eig, g.bins));
+        launch_pd_check(c->k, (int)g.m, (int)g.bins, c->flags + 3, c->flags + 4, min_eig, c->stream);
+        int rc = check_last_launch("pd_check_kernel");
+        if (!rc) rc = sync_flags(c, fl, 5);
+        if (!rc && (fl[3] != 0xffffffffu || fl[4] != 0xffffffffu)) {
+            // the reference checks bin by bin, Hermitian test first (gsvd.cpp:737-752)
             c->have_noise = false;
-            const bool herm_first = fl[3] <= fl[4];
-            const unsigned b = herm_first ? fl[3] : fl[4];
+            const unsigned b = std::min(fl[3], fl[4]);
+            const bool herm = fl[3] == b;
             if (bad_bin) *bad_bin = b;
-            return set_err(SSLG_NUMERICAL, std::string(herm_first ? "noise model is not Hermitian at bin "
-                                                                  : "noise model is not positive definite at bin ") +
-                                               std::to_string(b));
+            double ev = 0;
+            if (!herm) cudaMemcpy(&ev, min_eig + b, sizeof ev, cudaMemcpyDeviceToHost);
+            char buf[64];
+            std::snprintf(buf, sizeof buf, "%f", ev);  // std::to_string(double)
+            rc = set_err(SSLG_NUMERICAL, herm ? "noise model is not Hermitian at bin " + std::to_string(b)
+                                              : "noise model is not positive definite at bin " + std::to_string(b) +
+                                                    " (min eigenvalue " + buf + ")");
         }
+        cudaFree(min_eig);
+        TRY(rc);
     }
-    if (!g.pivoting)
-        return set_err(SSLG_VALIDATION, "pivot-free inversion is not supported by the device engine");
-    launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, c->kinv, c->flags + 1, c->flags + 2, c->stream);
+    launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, c->kinv, c->flags + 1, c->flags + 2, c->stream, g.pivoting);
     TRY(check_last_launch("gauss_jordan_kernel"));
     TRY(sync_flags(c, fl, 3));
     const unsigned bad = std::min(fl[1], fl[2]);
@@ -488,6 +570,35 @@ int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* ba
     }
     c->have_noise = true;
     return SSLG_OK;
+}
+
+int sslg_noise_inverse(sslg_ctx* c, int precision, double* out) {
+    if (!c || !out) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model inverses not prepared");
+    TRY(require_no_async(c));
+    CU(cudaSetDevice(c->cfg.device));
+    const sslg_config& g = c->cfg;
+    const size_t n = (size_t)g.bins * g.m * g.m;
+    if (precision) {
+        CU(cudaMemcpyAsync(out, c->kinv, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        return SSLG_OK;
+    }
+    // the float inverse is not kept by the engine (the solver is FP64): rebuild it
+    double2 *f = nullptr, *d = nullptr;
+    TRY(dalloc(&f, n));
+    int rc = dalloc(&d, n);
+    if (!rc) rc = reset_flags(c);
+    if (!rc) {
+        launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, d, c->flags + 1, c->flags + 2, c->stream, g.pivoting, f);
+        rc = check_last_launch("gauss_jordan_kernel");
+    }
+    if (!rc && cudaMemcpyAsync(out, f, n * sizeof(double2), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+        rc = set_err(SSLG_DEVICE, "cudaMemcpy failed");
+    if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = set_err(SSLG_DEVICE, "sync failed");
+    cudaFree(f);
+    if (d) cudaFree(d);
+    return rc;
 }
 
 int sslg_set_noise_identity(sslg_ctx* c) {
@@ -540,7 +651,9 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
                       const uint32_t* nbr) {
     if (!c || !h) return set_err(SSLG_VALIDATION, "null argument");
     if (dirs == 0) return set_err(SSLG_VALIDATION, "steering field has no directions");
+    TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
     const sslg_config& g = c->cfg;
     std::vector<uint32_t> off_own, nbr_own;
     if (!nbr_off) {
@@ -562,28 +675,52 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
     for (size_t i = 0; i < 2 * hn; ++i)
         if (!std::isfinite(h[i])) return set_err(SSLG_VALIDATION, "non-finite steering value");
     if (dirs != c->dirs) {
-        for (void* p : {(void*)c->h_raw, (void*)c->h_t, (void*)c->num, (void*)c->p, (void*)c->power,
-                        (void*)c->est_idx, (void*)c->est_pw, (void*)c->est_low})
-            if (p) cudaFree(p);
-        c->h_raw = c->h_t = nullptr;
-        c->num = c->p = c->power = c->est_pw = nullptr;
-        c->est_idx = nullptr;
-        c->est_low = nullptr;
+        // the new buffers are allocated first: on failure the context keeps
+        // its previous steering field intact
         const size_t NB = g.max_batch;
-        TRY(dalloc(&c->h_raw, hn));
-        TRY(dalloc(&c->h_t, hn));
-        TRY(dalloc(&c->num, (size_t)g.bins * dirs));
-        TRY(dalloc(&c->p, NB * g.bins * dirs));
-        TRY(dalloc(&c->power, NB * dirs));
-        TRY(dalloc(&c->est_idx, NB * g.num_sources));
-        TRY(dalloc(&c->est_pw, NB * g.num_sources));
-        TRY(dalloc(&c->est_low, NB * g.num_sources));
-        for (auto& sl : c->slots) {
-            if (sl.power) cudaFreeHost(sl.power);
-            sl.power = nullptr;
-            CU(cudaMallocHost(&sl.power, NB * dirs * sizeof(double)));
+        float2 *h_raw = nullptr, *h_t = nullptr;
+        double *num = nullptr, *p = nullptr, *power = nullptr, *est_pw = nullptr;
+        uint32_t* est_idx = nullptr;
+        uint8_t* est_low = nullptr;
+        double* slot_power[sslg_ctx::kSlots] = {};
+        int rc = 0;
+        rc |= dalloc(&h_raw, hn);
+        rc |= dalloc(&h_t, hn);
+        rc |= dalloc(&num, (size_t)g.bins * dirs);
+        rc |= dalloc(&p, NB * g.bins * dirs);
+        rc |= dalloc(&power, NB * dirs);
+        rc |= dalloc(&est_idx, NB * g.num_sources);
+        rc |= dalloc(&est_pw, NB * g.num_sources);
+        rc |= dalloc(&est_low, NB * g.num_sources);
+        for (int i = 0; i < sslg_ctx::kSlots && !rc; ++i)
+            if (cudaMallocHost(&slot_power[i], NB * dirs * sizeof(double)) != cudaSuccess)
+                rc = set_err(SSLG_DEVICE, "pinned result ring allocation failed");
+        if (rc) {
+            for (void* q : {(void*)h_raw, (void*)h_t, (void*)num, (void*)p, (void*)power, (void*)est_idx,
+                            (void*)est_pw, (void*)est_low})
+                if (q) cudaFree(q);
+            for (double* q : slot_power)
+                if (q) cudaFreeHost(q);
+            return rc;
+        }
+        CU(cudaStreamSynchronize(c->stream));  // nothing in flight may still use the old buffers
+        for (void* q : {(void*)c->h_raw, (void*)c->h_t, (void*)c->num, (void*)c->p, (void*)c->power,
+                        (void*)c->est_idx, (void*)c->est_pw, (void*)c->est_low})
+            if (q) cudaFree(q);
+        c->h_raw = h_raw;
+        c->h_t = h_t;
+        c->num = num;
+        c->p = p;
+        c->power = power;
+        c->est_idx = est_idx;
+        c->est_pw = est_pw;
+        c->est_low = est_low;
+        for (int i = 0; i < sslg_ctx::kSlots; ++i) {
+            if (c->slots[i].power) cudaFreeHost(c->slots[i].power);
+            c->slots[i].power = slot_power[i];
         }
         c->dirs = dirs;
+        c->last_emitted = 0;
     }
     if (c->nbr_off) cudaFree(c->nbr_off);
     if (c->nbr) cudaFree(c->nbr);
@@ -615,22 +752,44 @@ int sslg_reset_window(sslg_ctx* c) {
     for (auto& sl : c->slots) sl.pending = false;
     c->collected = c->next_id;
     c->poisoned = false;
+    c->dev_unverified.clear();
     return SSLG_OK;
 }
 
 int sslg_synchronize(sslg_ctx* c) {
     if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    CU(cudaSetDevice(c->cfg.device));
     CU(cudaStreamSynchronize(c->stream));
+    TRY(check_device_gate(c));
     return SSLG_OK;
 }
 
 int sslg_push_frames_device(sslg_ctx* c, const void* x_dev, uint32_t nframes, uint32_t* emitted) {
-    TRY(require_ready(c));
+    if (emitted) *emitted = 0;
+    TRY(require_ready(c, false));
     c->launches = 0;
     uint32_t total = 0;
     if (nframes > c->cfg.max_batch)
         return set_err(SSLG_VALIDATION, "push larger than max_batch; split it or raise max_batch");
-    TRY(stage_frames(c, static_cast<const float*>(x_dev), nframes, cudaMemcpyDeviceToDevice));
+    const sslg_config& g = c->cfg;
+    const size_t fsz = (size_t)g.m * g.bins;
+    const float* src = static_cast<const float*>(x_dev);
+    // stream-ordered: frames into the ring, the device-side non-finite gate
+    // (a failure makes every later kernel on the stream return early), the
+    // hot path -- no host synchronization; check_device_gate reports a failure
+    // at the next synchronizing call and rewinds the window to this push
+    const uint32_t seq = c->dev_seq++ & 0x7fffffffu;
+    c->dev_unverified.push_back({seq, c->pushed, c->since});
+    for (uint32_t done = 0; done < nframes;) {
+        const int slot = (int)((c->pushed + done) % c->cap);
+        const uint32_t run = std::min<uint32_t>(nframes - done, (uint32_t)(c->cap - slot));
+        CU(cudaMemcpyAsync(c->ring + (size_t)slot * fsz, src + (size_t)done * fsz * 2, run * fsz * sizeof(float2),
+                           cudaMemcpyDeviceToDevice, c->stream));
+        launch_gate_abort(reinterpret_cast<const float*>(c->ring + (size_t)slot * fsz), run * fsz * 2, c->abort, seq,
+                          c->stream);
+        ++c->launches;
+        done += run;
+    }
     TRY(process_chunk(c, nframes, &total));
     if (emitted) *emitted = total;
     return SSLG_OK;
@@ -641,6 +800,7 @@ int sslg_read_results(sslg_ctx* c, uint32_t n, sslg_block_out* blocks, uint32_t*
                       uint8_t* conv) {
     if (!c) return set_err(SSLG_VALIDATION, "null argument");
     CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
     if (n > c->last_emitted) return set_err(SSLG_VALIDATION, "fewer blocks available than requested");
     const sslg_config& g = c->cfg;
     const size_t ns = g.num_sources, D = c->dirs, B = g.bins;
@@ -654,7 +814,13 @@ int sslg_read_results(sslg_ctx* c, uint32_t n, sslg_block_out* blocks, uint32_t*
     if (sigma && n) CU(cudaMemcpyAsync(sigma, c->sigma, n * B * g.m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (sweeps && n) CU(cudaMemcpyAsync(sweeps, c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     if (conv && n) CU(cudaMemcpyAsync(conv, c->conv, n * B, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<uint32_t> sw_tmp;
+    if (conv && !sweeps && g.max_qr_sweeps && n) {
+        sw_tmp.resize(n * B);
+        CU(cudaMemcpyAsync(sw_tmp.data(), c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
     CU(cudaStreamSynchronize(c->stream));
+    apply_sweep_budget(g.max_qr_sweeps, sweeps ? sweeps : sw_tmp.data(), conv, sweeps || conv ? n * B : 0);
     if (blocks)
         for (uint32_t i = 0; i < n; ++i) {
             blocks[i].frame_index = (uint32_t)(c->last_first_frame + i);
@@ -665,6 +831,7 @@ int sslg_read_results(sslg_ctx* c, uint32_t n, sslg_block_out* blocks, uint32_t*
 
 int sslg_push_frames(sslg_ctx* c, const float* x, uint32_t nframes, sslg_block_out* blocks, uint32_t* est_idx,
                      double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    if (emitted) *emitted = 0;
     TRY(require_ready(c));
     const sslg_config& g = c->cfg;
     const size_t fsz = (size_t)g.m * g.bins * 2;
@@ -673,32 +840,49 @@ int sslg_push_frames(sslg_ctx* c, const float* x, uint32_t nframes, sslg_block_o
     while (done < nframes) {
         const uint32_t chunk = std::min<uint32_t>(nframes - done, g.max_batch);
         c->launches = 0;
-        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice));
+        uint32_t good = 0;
+        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice, &good));
+        // frames before the first non-finite one go through, as the
+        // reference's per-frame loop has pushed and sunk them before it throws
         uint32_t e = 0;
-        TRY(process_chunk(c, chunk, &e));
+        TRY(process_chunk(c, good, &e));
         launches += c->launches;
         TRY(sslg_read_results(c, e, blocks ? blocks + out : nullptr, est_idx ? est_idx + out * ns : nullptr,
                               est_power ? est_power + out * ns : nullptr, est_low ? est_low + out * ns : nullptr,
                               power ? power + (size_t)out * c->dirs : nullptr, nullptr, nullptr, nullptr, nullptr));
         out += e;
+        if (emitted) *emitted = out;
+        if (good < chunk) {
+            c->launches = launches;
+            return set_err(SSLG_VALIDATION, "non-finite spectrum value (frame " + std::to_string(done + good) + ")");
+        }
         done += chunk;
     }
     c->launches = launches;
-    if (emitted) *emitted = out;
     return SSLG_OK;
 }
 
 int sslg_correlation(sslg_ctx* c, const float* x, uint32_t nframes, float* r_out, uint32_t* emitted) {
+    if (emitted) *emitted = 0;
     if (!c || !x) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
     const sslg_config& g = c->cfg;
     const size_t fsz = (size_t)g.m * g.bins * 2;
     const size_t rsz = (size_t)g.bins * g.m * g.m;
     uint32_t out = 0, done = 0;
     c->launches = 0;
     while (done < nframes) {
-        const uint32_t chunk = std::min<uint32_t>(nframes - done, g.max_batch);
-        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice));
+        uint32_t chunk = std::min<uint32_t>(nframes - done, g.max_batch);
+        uint32_t good = 0;
+        TRY(stage_frames(c, x + done * fsz, chunk, cudaMemcpyHostToDevice, &good));
+        const bool bad = good < chunk;
+        chunk = good;
+        if (chunk == 0) {
+            if (emitted) *emitted = out;
+            return set_err(SSLG_VALIDATION, "non-finite spectrum value (frame " + std::to_string(done) + ")");
+        }
         const long long first_emit = std::max<long long>(0, (long long)g.window_frames - 1 - c->pushed);
         const int n = (int)std::max<long long>(0, (long long)chunk - first_emit);
         CorrArgs ca{c->ring, c->state, c->r, (int)g.m, (int)g.bins, (int)g.window_frames, c->cap, (int)chunk,
@@ -716,27 +900,59 @@ int sslg_correlation(sslg_ctx* c, const float* x, uint32_t nframes, float* r_out
         CU(cudaStreamSynchronize(c->stream));
         out += (uint32_t)n;
         done += chunk;
+        if (emitted) *emitted = out;
+        if (bad) return set_err(SSLG_VALIDATION, "non-finite spectrum value (frame " + std::to_string(done) + ")");
     }
-    if (emitted) *emitted = out;
     return SSLG_OK;
 }
 
 int sslg_gsvd(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, double* e, uint32_t* sweeps,
               uint8_t* conv) {
+    return sslg_gsvd_ex(c, r, nsets, sigma, e, nullptr, sweeps, conv, nullptr);
+}
+
+int sslg_gsvd_ex(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, double* e, double* er,
+                 uint32_t* sweeps, uint8_t* conv, double* resid) {
     if (!c || !r) return set_err(SSLG_VALIDATION, "null argument");
-    if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model not set");
+    TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
+    if (!c->have_noise) return set_err(SSLG_VALIDATION, "noise model not set");
     const sslg_config& g = c->cfg;
     const size_t mm = (size_t)g.m * g.m, B = g.bins;
     for (size_t i = 0; i < (size_t)nsets * B * mm * 2; ++i)
         if (!std::isfinite(r[i])) return set_err(SSLG_VALIDATION, "non-finite correlation entry");
     c->launches = 0;
+    const bool want_resid = resid && g.compute_residual;
+    std::vector<uint32_t> sw_tmp;
     for (uint32_t done = 0; done < nsets;) {
         const uint32_t n = std::min<uint32_t>(nsets - done, g.max_batch);
         CU(cudaMemcpyAsync(c->r, r + (size_t)done * B * mm * 2, n * B * mm * sizeof(float2), cudaMemcpyHostToDevice,
                            c->stream));
         CU(cudaEventRecord(c->ev[1], c->stream));
         TRY(run_gsvd(c, (int)n));
+        double* resid_dev = nullptr;
+        if (er || want_resid) {
+            // E_r (into e_tmp) and the residual, from the final E
+            if (want_resid) TRY(dalloc(&resid_dev, n * B));
+            ErArgs ea{c->r, c->kinv, c->sigma, c->e, er ? c->e_tmp : nullptr, resid_dev, (int)g.m, (int)g.bins};
+            launch_er(ea, (int)n, c->stream);
+            ++c->launches;
+            int rc = check_last_launch("er_kernel");
+            if (!rc && er &&
+                cudaMemcpyAsync(er + (size_t)done * B * mm * 2, c->e_tmp, n * B * mm * sizeof(double2),
+                                cudaMemcpyDeviceToHost, c->stream) != cudaSuccess)
+                rc = set_err(SSLG_DEVICE, "cudaMemcpy failed");
+            if (!rc && want_resid &&
+                cudaMemcpyAsync(resid + (size_t)done * B, resid_dev, n * B * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream) != cudaSuccess)
+                rc = set_err(SSLG_DEVICE, "cudaMemcpy failed");
+            if (!rc && cudaStreamSynchronize(c->stream) != cudaSuccess) rc = set_err(SSLG_DEVICE, "sync failed");
+            if (resid_dev) cudaFree(resid_dev);
+            TRY(rc);
+        }
+        if (resid && !want_resid)
+            for (size_t i = 0; i < n * B; ++i) resid[done * B + i] = -1.0;  // recon_residual < 0: not computed
         if (e) {
             const size_t tot = n * B * mm;
             transpose_sq_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, c->stream>>>(c->e, c->e_tmp, (int)g.m, n * B);
@@ -748,11 +964,15 @@ int sslg_gsvd(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, double
         if (sigma)
             CU(cudaMemcpyAsync(sigma + (size_t)done * B * g.m, c->sigma, n * B * g.m * sizeof(double),
                                cudaMemcpyDeviceToHost, c->stream));
-        if (sweeps)
-            CU(cudaMemcpyAsync(sweeps + (size_t)done * B, c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                               c->stream));
+        uint32_t* swp = sweeps ? sweeps + (size_t)done * B : nullptr;
+        if (!swp && conv && g.max_qr_sweeps) {
+            sw_tmp.resize(n * B);
+            swp = sw_tmp.data();
+        }
+        if (swp) CU(cudaMemcpyAsync(swp, c->sweeps, n * B * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
         if (conv) CU(cudaMemcpyAsync(conv + (size_t)done * B, c->conv, n * B, cudaMemcpyDeviceToHost, c->stream));
         CU(cudaStreamSynchronize(c->stream));
+        apply_sweep_budget(g.max_qr_sweeps, swp, conv ? conv + (size_t)done * B : nullptr, n * B);
         done += n;
     }
     return SSLG_OK;
@@ -760,6 +980,8 @@ int sslg_gsvd(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, double
 
 int sslg_spectrum(sslg_ctx* c, const double* e, uint32_t nsets, double* power, double* bin_power) {
     if (!c || !e) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(require_no_async(c));
+    TRY(check_device_gate(c));
     if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
     if (c->cfg.num_sources >= c->cfg.m)
         return set_err(SSLG_VALIDATION, "num_sources must be smaller than the channel count");
@@ -791,6 +1013,8 @@ int sslg_spectrum(sslg_ctx* c, const double* e, uint32_t nsets, double* power, d
 int sslg_peaks(sslg_ctx* c, const double* power, uint32_t nsets, uint32_t* est_idx, double* est_power,
                uint8_t* est_low, uint32_t* count) {
     if (!c || !power) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(require_no_async(c));
+    TRY(check_device_gate(c));
     if (!c->have_steering) return set_err(SSLG_VALIDATION, "steering field not set");
     CU(cudaSetDevice(c->cfg.device));
     const sslg_config& g = c->cfg;
@@ -1015,6 +1239,7 @@ int sslg_samples_pending(const sslg_ctx* c, uint64_t nsamples, uint32_t* frames,
 
 int sslg_push_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32_t cap_blocks, sslg_block_out* blocks,
                       uint32_t* est_idx, double* est_power, uint8_t* est_low, double* power, uint32_t* emitted) {
+    if (emitted) *emitted = 0;
     TRY(require_ready(c));
     if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
     if (!pcm && nsamples) return set_err(SSLG_VALIDATION, "null argument");
@@ -1035,18 +1260,25 @@ int sslg_push_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32_t
             continue;
         }
         TRY(launch_stft_frames(c, c->samp[c->samp_cur], c->samp_cap, (int)nf, c->ring, c->cap, c->pushed));
-        TRY(gate_frames(c, nf));
+        uint32_t good = 0;
+        TRY(gate_frames(c, nf, &good));
+        // frames before the first non-finite one go through (run_locate has
+        // pushed and sunk them when the bad frame throws, pipeline.cpp:227-245)
         uint32_t e = 0;
-        TRY(process_chunk(c, nf, &e));
-        TRY(consume_samples(c, (size_t)nf * c->stft.shift));
+        TRY(process_chunk(c, good, &e));
+        TRY(consume_samples(c, (size_t)good * c->stft.shift));
         launches += c->launches;
         TRY(sslg_read_results(c, e, blocks ? blocks + out : nullptr, est_idx ? est_idx + out * ns : nullptr,
                               est_power ? est_power + out * ns : nullptr, est_low ? est_low + out * ns : nullptr,
                               power ? power + (size_t)out * c->dirs : nullptr, nullptr, nullptr, nullptr, nullptr));
         out += e;
+        if (emitted) *emitted = out;
+        if (good < nf) {
+            c->launches = launches;
+            return set_err(SSLG_VALIDATION, "non-finite spectrum value (frame " + std::to_string(c->pushed) + ")");
+        }
     }
     c->launches = launches;
-    if (emitted) *emitted = out;
     return SSLG_OK;
 }
 
@@ -1060,11 +1292,28 @@ int sslg_locate_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32
 
 // ---- asynchronous streaming --------------------------------
 
+int sslg_set_async_power(sslg_ctx* c, int on) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    TRY(require_no_async(c));
+    c->async_power = on != 0;
+    return SSLG_OK;
+}
+
 int sslg_push_samples_async(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint64_t* ticket) {
-    TRY(require_ready(c));
+    if (!c) return set_err(SSLG_VALIDATION, "null context");
+    {
+        // asynchronous pushes may queue behind each other: only the
+        // collected-vs-enqueued check of require_ready is skipped here
+        const uint64_t nid = c->next_id, col = c->collected;
+        c->collected = nid;
+        const int rc = require_ready(c);
+        c->collected = col;
+        TRY(rc);
+    }
     if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
     if (!pcm && nsamples) return set_err(SSLG_VALIDATION, "null argument");
     if (c->poisoned) return set_err(SSLG_VALIDATION, "stream stopped by a non-finite spectrum value; reset the window");
+    TRY(check_device_gate(c));
     uint32_t frames = 0;
     TRY(sslg_samples_pending(c, nsamples, &frames, nullptr));
     const uint32_t subs = (frames + c->cfg.max_batch - 1) / c->cfg.max_batch;
@@ -1107,8 +1356,9 @@ int sslg_push_samples_async(sslg_ctx* c, const float* pcm, uint64_t nsamples, ui
             CU(cudaMemcpyAsync(sl.pw, c->est_pw, e * ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
             CU(cudaMemcpyAsync(sl.low, c->est_low, e * ns, cudaMemcpyDeviceToHost, c->stream));
             CU(cudaMemcpyAsync(sl.cnt, c->est_count, e * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-            CU(cudaMemcpyAsync(sl.power, c->power, (size_t)e * c->dirs * sizeof(double), cudaMemcpyDeviceToHost,
-                               c->stream));
+            if (c->async_power)
+                CU(cudaMemcpyAsync(sl.power, c->power, (size_t)e * c->dirs * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
         }
         CU(cudaEventRecord(sl.done, c->stream));
         sl.pending = true;
@@ -1130,6 +1380,18 @@ int sslg_wait_results(sslg_ctx* c, uint64_t ticket, uint32_t cap_blocks, sslg_bl
     if (ticket > c->collected) CU(cudaEventSynchronize(c->slots[(ticket - 1) % sslg_ctx::kSlots].done));
     unsigned int ab = 0;
     CU(cudaMemcpy(&ab, c->abort, sizeof ab, cudaMemcpyDeviceToHost));
+    // the whole requested range must fit before any slot is consumed
+    {
+        uint64_t total = 0;
+        for (uint64_t id = c->collected; id < ticket; ++id) {
+            const auto& sl = c->slots[id % sslg_ctx::kSlots];
+            if (ab && sl.id + 1 >= ab) break;
+            total += sl.n;
+        }
+        if (total > cap_blocks) return set_err(SSLG_VALIDATION, "result arrays too small for the emitted blocks");
+    }
+    if (power && !c->async_power)
+        return set_err(SSLG_VALIDATION, "power was not requested for asynchronous pushes (sslg_set_async_power)");
     uint32_t out = 0;
     while (c->collected < ticket) {
         auto& sl = c->slots[c->collected % sslg_ctx::kSlots];
@@ -1146,7 +1408,6 @@ int sslg_wait_results(sslg_ctx* c, uint64_t ticket, uint32_t cap_blocks, sslg_bl
             if (emitted) *emitted = out;
             return set_err(SSLG_VALIDATION, "non-finite spectrum value");
         }
-        if (out + sl.n > cap_blocks) return set_err(SSLG_VALIDATION, "result arrays too small for the emitted blocks");
         for (uint32_t b = 0; b < sl.n; ++b) {
             if (blocks) {
                 blocks[out + b].frame_index = (uint32_t)(sl.first_frame + b);

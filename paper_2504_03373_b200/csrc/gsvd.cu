@@ -1104,7 +1104,7 @@ __device__ __forceinline__ void japply(double2 (&P)[RPL], double2 (&Q)[RPL], con
 // column.  Returns whether a rotation was applied.
 template <int R, int L>
 __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], double& cp, double& cq, double drop,
-                                            int s, int m, double& maxrel) {
+                                            int s, int m, double& maxrel, double tol2) {
     double d0x = 0, d0y = 0, d1x = 0, d1y = 0;
 #pragma unroll
     for (int u = 0; u < R; ++u) {
@@ -1120,7 +1120,7 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
     }
     const double2 dot = group_sum2<L>(make_double2(d0x + d1x, d0y + d1y));
     const double mag2 = fma(dot.x, dot.x, dot.y * dot.y);
-    if (cp <= drop || cq <= drop || mag2 <= 1e-28 * cp * cq) return false;
+    if (cp <= drop || cq <= drop || mag2 <= tol2 * cp * cq) return false;
     if (mag2 > 1e-16 * cp * cq) maxrel = 1.0;  // a coupling above 1e-8 relative was rotated
     japply<R>(P, Q, jrot(dot.x, dot.y, cp, cq), cp, cq);
     return true;
@@ -1132,7 +1132,7 @@ __device__ __forceinline__ bool rotate_pair(double2 (&P)[R], double2 (&Q)[R], do
 // one 4x4-register-tiled Gram product over the upper triangle instead of a
 // full verification sweep of round-synchronized pair visits.
 template <int MC, int TS = 2>  // 2x2 tiles keep the fused kernel's register budget
-__device__ bool gram_converged(const double2* W, int m_rt, const double* cn, double drop) {
+__device__ bool gram_converged(const double2* W, int m_rt, const double* cn, double drop, double tol2) {
     const int m = MC > 0 ? MC : m_rt;
     const int nt = (m + TS - 1) / TS;
     const int ntiles = nt * (nt + 1) / 2;
@@ -1176,7 +1176,7 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
                 const int p = p0 + u, q = q0 + v;
                 if (p < q && q < m && cn[p] > drop && cn[q] > drop) {
                     const double mag2 = fma(acc[u][v].x, acc[u][v].x, acc[u][v].y * acc[u][v].y);
-                    if (mag2 > 1e-28 * cn[p] * cn[q]) bad = true;
+                    if (mag2 > tol2 * cn[p] * cn[q]) bad = true;
                 }
             }
     }
@@ -1305,7 +1305,7 @@ __device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const Gs
         // rotation-free in 98% of bins), or only pairs coupled by <= 1e-8
         // relative, is usually rotation-free: certify that with one Gram
         // product instead of running it (7.44 -> 7.06 sweeps at C3).
-        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC, LPP == 4 ? 4 : 2>(W, m, cn, drop)) {
+        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC, LPP == 4 ? 4 : 2>(W, m, cn, drop, a.tol2)) {
             converged = true;
             break;
         }
@@ -1331,7 +1331,7 @@ __device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const Gs
                         Q[u] = row < m ? W[q * m + row] : make_double2(0, 0);
                     }
                     double cp = cn[p], cq = cn[q];
-                    if (rotate_pair<RW, LPP>(P, Q, cp, cq, drop, s, m, mymax)) {
+                    if (rotate_pair<RW, LPP>(P, Q, cp, cq, drop, s, m, mymax, a.tol2)) {
 #pragma unroll
                         for (int u = 0; u < RW; ++u) {
                             const int row = s + u * LPP;

@@ -31,13 +31,20 @@ struct CorrArgs {
 };
 void launch_correlation(const CorrArgs& a, cudaStream_t s);
 void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStream_t s);
+// synchronous per-frame gate: min(frame0 + f) over frames f holding a non-finite value -> *first
+void launch_first_nonfinite(const float* p, size_t per_frame, int nframes, unsigned int frame0, unsigned int* first,
+                            cudaStream_t s);
 // async gate: the first failing push id + 1 lands in *abort (atomicCAS from 0)
 void launch_gate_abort(const float* p, size_t n, unsigned int* abort, unsigned int id, cudaStream_t s);
 
+// mat_inverse<float> and mat_inverse<double> (gsvd.cpp:21-62) of every bin:
+// inv_out <- the double inverse, inv_f_out (nullable) <- the float inverse widened
 void launch_gauss_jordan(const float2* k, int m, int bins, double2* inv_out, unsigned int* bad_f,
-                         unsigned int* bad_d, cudaStream_t s);
+                         unsigned int* bad_d, cudaStream_t s, int pivoting = 1, double2* inv_f_out = nullptr);
+// check_positive_definite (gsvd.cpp:736-754): Hermitian test + smallest eigenvalue
+// of hermitian_eigenvalues (eig.cpp:11-84) per bin into min_eig (nullable)
 void launch_pd_check(const float2* k, int m, int bins, unsigned int* bad_herm, unsigned int* bad_pd,
-                     double* min_pivot, cudaStream_t s);
+                     double* min_eig, cudaStream_t s);
 
 struct GsvdArgs {
     const float2* r;      // [nblk][bins][m][m] row-major R
@@ -55,6 +62,8 @@ struct GsvdArgs {
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
     double2* wscratch = nullptr;  // [nblk][bins][m][m] W between the split solver kernels (m = 60)
     int* pivs = nullptr;          // [nblk][bins][64] QR column pivots between them
+    double tol2 = 1e-28;          // no-rotation test |a_pq|^2 <= tol2 |w_p|^2 |w_q|^2 (gsvd.cpp:648);
+                                  // 1e-28 * SolverConfig::tolerance_scale^2
 };
 // returns the number of kernels launched (1, or 3 when the solver is split
 // around a 128-thread sweep kernel)
@@ -70,6 +79,19 @@ struct CanonArgs {
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_canonical(const CanonArgs& a, int nblk, cudaStream_t s);
+
+// E_r rows and the reconstruction residual from the final E (er.cu)
+struct ErArgs {
+    const float2* r;      // [nblk][bins][m][m]
+    const double2* kinv;  // [bins][m][m]
+    const double* sigma;  // [nblk][bins][m]
+    const double2* e;     // [nblk][bins][m vec][m row]
+    double2* er;          // [nblk][bins][m][m] row-major (nullable)
+    double* resid;        // [nblk][bins] (nullable)
+    int m, bins;
+    const unsigned int* abort = nullptr;
+};
+void launch_er(const ErArgs& a, int nblk, cudaStream_t s);
 
 struct SpecArgs {
     const double2* e;    // [nblk][bins][m vec][m mic]

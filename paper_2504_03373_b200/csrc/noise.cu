@@ -8,11 +8,17 @@
 // here so the error behaviour matches, and the FP64 inverse is kept for the
 // solver.  One CTA per bin, the augmented [K | I] block resident in SMEM.
 //
+// The elimination's arithmetic is the reference's, operation for operation:
+// std::complex products and the division 1/a(col,col) in the limited-range
+// textbook form the reference is built with (-fcx-limited-range), every
+// product and sum rounded on its own (no FMA contraction: x86-64 baseline
+// code has none), so both inverses are bit-identical to mat_inverse<T>.
+//
 // PD gate (NoiseModel::check_positive_definite, gsvd.cpp:736-754): the
-// Hermitian test is reproduced as written; "smallest eigenvalue > 0" is
-// decided by an FP64 Cholesky (a Hermitian matrix is positive definite iff
-// its Cholesky pivots are all positive) instead of a full Jacobi
-// eigensolve.
+// Hermitian test as written, then the smallest eigenvalue of the FP64
+// widening from the reference's own cyclic complex Jacobi
+// (hermitian_eigenvalues, eig.cpp:11-84: same pair order, same stop rule,
+// same rotation formulas and rounding), one warp per bin.
 #include "common.cuh"
 
 namespace sslg {
@@ -36,6 +42,34 @@ template <>
 __device__ __forceinline__ double cabs_t<double>(double re, double im) { return hypot(re, im); }
 
 template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T sub_rn(T a, T b);
+template <>
+__device__ __forceinline__ float sub_rn<float>(float a, float b) { return __fsub_rn(a, b); }
+template <>
+__device__ __forceinline__ double sub_rn<double>(double a, double b) { return __dsub_rn(a, b); }
+
+// std::complex<T> product, limited-range form (a*c - b*d, a*d + b*c)
+template <typename C, typename T>
+__device__ __forceinline__ C cmul_rn(C a, C b) {
+    C r;
+    r.x = sub_rn<T>(mul_rn<T>(a.x, b.x), mul_rn<T>(a.y, b.y));
+    r.y = add_rn<T>(mul_rn<T>(a.x, b.y), mul_rn<T>(a.y, b.x));
+    return r;
+}
+
+template <typename T>
 __device__ __forceinline__ T eps_t();
 template <>
 __device__ __forceinline__ float eps_t<float>() { return 1.1920928955078125e-07f; }
@@ -48,7 +82,7 @@ constexpr int kInvThreads = 256;
 template <typename T>
 __global__ void __launch_bounds__(kInvThreads) gauss_jordan_kernel(const float2* __restrict__ k, int m,
                                                                     double2* __restrict__ inv_out,
-                                                                    unsigned int* bad_bin) {
+                                                                    unsigned int* bad_bin, int pivoting) {
     using C = typename cplx_t<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C* aug = reinterpret_cast<C*>(smem_raw);
@@ -93,8 +127,14 @@ __global__ void __launch_bounds__(kInvThreads) gauss_jordan_kernel(const float2*
     const T floor_ = s_scale * eps_t<T>() * (T)m;
 
     for (int col = 0; col < m; ++col) {
-        // partial pivoting: first row with the largest magnitude
-        if (tid < 32) {
+        if (!pivoting) {  // Pivoting::none: the diagonal entry or give up (gsvd.cpp:33-39)
+            if (tid == 0) {
+                const C v = aug[col * w + col];
+                s_piv = col;
+                if (!(cabs_t<T>(v.x, v.y) > floor_)) s_fail = 1;
+            }
+        } else if (tid < 32) {
+            // partial pivoting: first row with the largest magnitude
             T best = -1;
             int bi = col;
             for (int r = col + tid; r < m; r += 32) {
@@ -128,20 +168,15 @@ __global__ void __launch_bounds__(kInvThreads) gauss_jordan_kernel(const float2*
                 aug[piv * w + j] = t0;
             }
         __syncthreads();
-        // d = 1 / a(col, col) with the textbook complex division
+        // d = (1, 0) / a(col, col), limited-range division:
+        // ((1*x + 0*y) / den, (0*x - 1*y) / den), den = x*x + y*y
         const C p = aug[col * w + col];
-        const T den = p.x * p.x + p.y * p.y;
+        const T den = add_rn<T>(mul_rn<T>(p.x, p.x), mul_rn<T>(p.y, p.y));
         C d;
-        d.x = p.x / den;
-        d.y = -p.y / den;
+        d.x = add_rn<T>(p.x, mul_rn<T>((T)0, p.y)) / den;
+        d.y = sub_rn<T>(mul_rn<T>((T)0, p.x), p.y) / den;
         __syncthreads();
-        for (int j = tid; j < w; j += blockDim.x) {
-            const C v = aug[col * w + j];
-            C r;
-            r.x = v.x * d.x - v.y * d.y;
-            r.y = v.x * d.y + v.y * d.x;
-            aug[col * w + j] = r;
-        }
+        for (int j = tid; j < w; j += blockDim.x) aug[col * w + j] = cmul_rn<C, T>(aug[col * w + j], d);
         for (int r = tid; r < m; r += blockDim.x) s_f[r] = aug[r * w + col];
         __syncthreads();
         for (int e = tid; e < m * w; e += blockDim.x) {
@@ -149,10 +184,10 @@ __global__ void __launch_bounds__(kInvThreads) gauss_jordan_kernel(const float2*
             if (r == col) continue;
             const C f = s_f[r];
             if (f.x == (T)0 && f.y == (T)0) continue;
-            const C pv = aug[col * w + j];
+            const C pr = cmul_rn<C, T>(f, aug[col * w + j]);
             C v = aug[e];
-            v.x -= f.x * pv.x - f.y * pv.y;
-            v.y -= f.x * pv.y + f.y * pv.x;
+            v.x = sub_rn<T>(v.x, pr.x);
+            v.y = sub_rn<T>(v.y, pr.y);
             aug[e] = v;
         }
         __syncthreads();
@@ -169,81 +204,118 @@ __global__ void __launch_bounds__(kInvThreads) gauss_jordan_kernel(const float2*
         }
 }
 
-// Hermitian test + FP64 Cholesky.  bad_herm / bad_pd receive the first bad bin.
-__global__ void __launch_bounds__(kInvThreads) pd_check_kernel(const float2* __restrict__ k, int m,
-                                                                unsigned int* bad_herm, unsigned int* bad_pd,
-                                                                double* min_pivot) {
+// Hermitian test + hermitian_eigenvalues (eig.cpp:11-84) on the FP64
+// widening, one warp per bin (the matrix in shared memory).  The rotation
+// sequence is the reference's -- pairs (p, q) in row-major order, skipped
+// when |a_pq| <= 1e-14 max|a|, at most 60 sweeps -- and within a rotation the
+// column pair is updated for every row, then the row pair for every column,
+// each element with the reference's rounding; lanes split the rows/columns.
+// bad_herm / bad_pd receive the first bad bin, min_eig[b] the smallest
+// eigenvalue (NaN when the Hermitian test fails).
+__device__ __forceinline__ double2 cmul_d(double2 a, double2 b) { return cmul_rn<double2, double>(a, b); }
+__device__ __forceinline__ double2 rscale_d(double s, double2 a) {  // real * complex
+    return make_double2(__dmul_rn(s, a.x), __dmul_rn(s, a.y));
+}
+
+__global__ void __launch_bounds__(32) pd_check_kernel(const float2* __restrict__ k, int m, unsigned int* bad_herm,
+                                                      unsigned int* bad_pd, double* min_eig) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* a = reinterpret_cast<double2*>(smem_raw);  // [m][m]
-    __shared__ int s_fail;
-    __shared__ double s_piv;
+    double2* a = reinterpret_cast<double2*>(smem_raw);  // [m][m] row-major
     const int b = blockIdx.x;
-    const int tid = threadIdx.x;
+    const int lane = threadIdx.x;
     const float2* kb = k + (size_t)b * m * m;
-    if (tid < 32) {
-        double scale = 0, herm = 0;
-        for (int e = tid; e < m * m; e += 32) {
-            const int i = e / m, j = e % m;
-            const float2 v = kb[i * m + j];
-            const float2 u = kb[j * m + i];
-            scale = fmax(scale, (double)hypotf(v.x, v.y));
-            herm = fmax(herm, (double)hypotf(v.x - u.x, v.y + u.y));
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
-            herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
-        }
-        if (tid == 0) s_fail = herm > 1e-5 * scale + 1e-30 ? 1 : 0;
+    double scale = 0, herm = 0, amax = 0;
+    for (int e = lane; e < m * m; e += 32) {
+        const int i = e / m, j = e % m;
+        const float2 v = kb[i * m + j];
+        const float2 u = kb[j * m + i];
+        scale = fmax(scale, (double)hypotf(v.x, v.y));
+        herm = fmax(herm, (double)hypotf(v.x - u.x, v.y + u.y));
+        a[e] = f2d(v);
+        amax = fmax(amax, hypot((double)v.x, (double)v.y));
     }
-    for (int e = tid; e < m * m; e += blockDim.x) a[e] = f2d(kb[e]);
-    __syncthreads();
-    if (s_fail) {
-        if (tid == 0) atomicMin(bad_herm, (unsigned)b);
+    for (int o = 16; o > 0; o >>= 1) {
+        scale = fmax(scale, __shfl_xor_sync(0xffffffffu, scale, o));
+        herm = fmax(herm, __shfl_xor_sync(0xffffffffu, herm, o));
+        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    __syncwarp();
+    if (herm > 1e-5 * scale + 1e-30) {
+        if (lane == 0) {
+            atomicMin(bad_herm, (unsigned)b);
+            if (min_eig) min_eig[b] = __longlong_as_double(0x7ff8000000000000ll);
+        }
         return;
     }
-    // right-looking Cholesky on the lower triangle
-    for (int c = 0; c < m; ++c) {
-        if (tid == 0) {
-            const double d = a[c * m + c].x;
-            s_piv = d;
-            if (!(d > 0)) s_fail = 1;
+    const double stop = 1e-14 * (amax > 0 ? amax : 1.0);
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        bool rotated = false;
+        for (int p = 0; p + 1 < m; ++p) {
+            for (int q = p + 1; q < m; ++q) {
+                const double2 apq = a[p * m + q];
+                const double mag = hypot(apq.x, apq.y);
+                if (mag <= stop) continue;  // warp-uniform (every lane reads the same entry)
+                rotated = true;
+                const double2 ph = make_double2(apq.x / mag, apq.y / mag);
+                const double app = a[p * m + p].x;
+                const double aqq = a[q * m + q].x;
+                const double tau = __dsub_rn(aqq, app) / __dmul_rn(2.0, mag);
+                const double t = (tau >= 0 ? 1.0 : -1.0) /
+                                 __dadd_rn(fabs(tau), sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau))));
+                const double c = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(t, t)));
+                const double s = __dmul_rn(t, c);
+                const double2 sphc = rscale_d(s, cconj(ph));  // s * conj(ph)
+                const double2 sph = rscale_d(s, ph);          // s * ph
+                __syncwarp();
+                for (int i = lane; i < m; i += 32) {  // columns p, q
+                    const double2 aip = a[i * m + p], aiq = a[i * m + q];
+                    const double2 x = rscale_d(c, aip), y = cmul_d(sphc, aiq);
+                    const double2 u = cmul_d(sph, aip), v = rscale_d(c, aiq);
+                    a[i * m + p] = make_double2(__dsub_rn(x.x, y.x), __dsub_rn(x.y, y.y));
+                    a[i * m + q] = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
+                }
+                __syncwarp();
+                for (int j = lane; j < m; j += 32) {  // rows p, q
+                    const double2 apj = a[p * m + j], aqj = a[q * m + j];
+                    const double2 x = rscale_d(c, apj), y = cmul_d(sph, aqj);
+                    const double2 u = cmul_d(sphc, apj), v = rscale_d(c, aqj);
+                    a[p * m + j] = make_double2(__dsub_rn(x.x, y.x), __dsub_rn(x.y, y.y));
+                    a[q * m + j] = make_double2(__dadd_rn(u.x, v.x), __dadd_rn(u.y, v.y));
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    a[p * m + p].y = 0.0;
+                    a[q * m + q].y = 0.0;
+                }
+                __syncwarp();
+            }
         }
-        __syncthreads();
-        if (s_fail) break;
-        const double rs = rsqrt(s_piv);
-        for (int r = c + 1 + tid; r < m; r += blockDim.x) a[r * m + c] = cscale(rs, a[r * m + c]);
-        __syncthreads();
-        const int n = m - c - 1;
-        for (int e = tid; e < n * n; e += blockDim.x) {
-            const int r = c + 1 + e / n, j = c + 1 + e % n;
-            if (j > r) continue;
-            // a(r, j) -= l(r, c) * conj(l(j, c))
-            const double2 lr = a[r * m + c], lj = a[j * m + c];
-            a[r * m + j] = csub(a[r * m + j], cmul(lr, cconj(lj)));
-        }
-        __syncthreads();
+        if (!rotated) break;
     }
-    if (tid == 0) {
-        if (s_fail) atomicMin(bad_pd, (unsigned)b);
-        if (min_pivot) min_pivot[b] = s_piv;
+    double mn = INFINITY;
+    for (int i = lane; i < m; i += 32) mn = fmin(mn, a[i * m + i].x);
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) {
+        if (!(mn > 0)) atomicMin(bad_pd, (unsigned)b);  // eig.back() > 0 (gsvd.cpp:746-747)
+        if (min_eig) min_eig[b] = mn;
     }
 }
 
 void launch_gauss_jordan(const float2* k, int m, int bins, double2* inv_out, unsigned int* bad_f,
-                         unsigned int* bad_d, cudaStream_t s) {
+                         unsigned int* bad_d, cudaStream_t s, int pivoting, double2* inv_f_out) {
     const size_t smem_f = (size_t)m * 2 * m * sizeof(float2);
     const size_t smem_d = (size_t)m * 2 * m * sizeof(double2);
     cudaFuncSetAttribute(gauss_jordan_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
     cudaFuncSetAttribute(gauss_jordan_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
-    gauss_jordan_kernel<float><<<bins, kInvThreads, smem_f, s>>>(k, m, nullptr, bad_f);
-    gauss_jordan_kernel<double><<<bins, kInvThreads, smem_d, s>>>(k, m, inv_out, bad_d);
+    gauss_jordan_kernel<float><<<bins, kInvThreads, smem_f, s>>>(k, m, inv_f_out, bad_f, pivoting);
+    gauss_jordan_kernel<double><<<bins, kInvThreads, smem_d, s>>>(k, m, inv_out, bad_d, pivoting);
 }
 
 void launch_pd_check(const float2* k, int m, int bins, unsigned int* bad_herm, unsigned int* bad_pd,
-                     double* min_pivot, cudaStream_t s) {
+                     double* min_eig, cudaStream_t s) {
     const size_t smem = (size_t)m * m * sizeof(double2);
     cudaFuncSetAttribute(pd_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    pd_check_kernel<<<bins, kInvThreads, smem, s>>>(k, m, bad_herm, bad_pd, min_pivot);
+    pd_check_kernel<<<bins, 32, smem, s>>>(k, m, bad_herm, bad_pd, min_eig);
 }
 
 }  // namespace sslg

@@ -189,7 +189,8 @@ class GsvdBatch:
     e: np.ndarray
     iterations: np.ndarray
     converged: np.ndarray
-    e_r: Optional[np.ndarray] = None
+    e_r: Optional[np.ndarray] = None  # [B][m][m], row i pairs with value i
+    recon_residual: Optional[np.ndarray] = None  # [B]; -1 unless SolverConfig.compute_residual
 
     @property
     def bins(self) -> int:
@@ -250,6 +251,9 @@ class Engine:
         cfg.canonical_subspaces = int(solver.canonical_subspaces)
         cfg.refine_leading = int(solver.refine_leading)
         cfg.precondition = int(solver.precondition)
+        cfg.max_qr_sweeps = int(solver.max_qr_sweeps)
+        cfg.tolerance_scale = float(solver.tolerance_scale)
+        cfg.compute_residual = int(solver.compute_residual)
         cfg.max_batch = max_batch
         cfg.device = device
         cfg.stream = stream
@@ -316,12 +320,9 @@ class Engine:
         low = np.zeros((n_max, ns), np.uint8)
         power = np.zeros((n_max, self.dirs)) if want_power else None
         em = C.c_uint32()
-        _capi.check(self.L.sslg_push_frames(self.h, f32p(frames), f, blocks, u32p(idx), f64p(pw), u8p(low),
-                                            f64p(power), C.byref(em)))
-        n = em.value
-        return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
-                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
-                    low=low[:n].astype(bool), power=None if power is None else power[:n])
+        rc = self.L.sslg_push_frames(self.h, f32p(frames), f, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
+                                     C.byref(em))
+        return _blocks_result(rc, em.value, blocks, idx, pw, low, power)
 
     # ---- STFT front end (SampleBlock in) -----------------------------------
     def set_stft(self, stft: "StftConfig") -> None:
@@ -362,12 +363,9 @@ class Engine:
         low = np.zeros((cap, ns), np.uint8)
         power = np.zeros((cap, self.dirs)) if want_power else None
         em = C.c_uint32()
-        _capi.check(fn(self.h, f32p(pcm), pcm.shape[1], cap, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
-                       C.byref(em)))
-        n = em.value
-        return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
-                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
-                    low=low[:n].astype(bool), power=None if power is None else power[:n])
+        rc = fn(self.h, f32p(pcm), pcm.shape[1], cap, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
+                C.byref(em))
+        return _blocks_result(rc, em.value, blocks, idx, pw, low, power)
 
     def push_samples(self, pcm: np.ndarray, want_power: bool = False):
         """Streaming: appends pcm [m][n] float32 to the sample history and runs
@@ -391,6 +389,11 @@ class Engine:
         self._inflight = getattr(self, "_inflight", [])
         self._inflight.append((t.value, pcm))
         return t.value
+
+    def set_async_power(self, on: bool = True) -> None:
+        """Asynchronous pushes also bring the broadband power back (for
+        wait_results(want_power=True))."""
+        _capi.check(self.L.sslg_set_async_power(self.h, int(on)))
 
     def wait_results(self, ticket: int, cap: int = 4096, want_power: bool = False):
         """Blocks of every asynchronous push up to `ticket`, in order."""
@@ -465,7 +468,9 @@ class Engine:
         _capi.check(self.L.sslg_correlation(self.h, f32p(frames), f, f32p(out), C.byref(em)))
         return out[: em.value]
 
-    def gsvd(self, r: np.ndarray):
+    def gsvd(self, r: np.ndarray, want_er: bool = False, want_resid: bool = False):
+        """sigma [n][B][m], E [n][B][m][m], sweeps, converged (+ E_r and the
+        residual when asked: sslg_gsvd_ex)."""
         r = c64(r)
         if r.ndim == 3:
             r = r[None]
@@ -474,10 +479,21 @@ class Engine:
             raise ValidationError("noise model bin count does not match correlation set")
         sigma = np.zeros((n, self.bins, self.m))
         e = np.zeros((n, self.bins, self.m, self.m), np.complex128)
+        er = np.zeros((n, self.bins, self.m, self.m), np.complex128) if want_er else None
+        res = np.zeros((n, self.bins)) if want_resid else None
         sw = np.zeros((n, self.bins), np.uint32)
         cv = np.zeros((n, self.bins), np.uint8)
-        _capi.check(self.L.sslg_gsvd(self.h, f32p(r), n, f64p(sigma), f64p(e), u32p(sw), u8p(cv)))
+        _capi.check(self.L.sslg_gsvd_ex(self.h, f32p(r), n, f64p(sigma), f64p(e), f64p(er), u32p(sw), u8p(cv),
+                                        f64p(res)))
+        if want_er or want_resid:
+            return sigma, e, sw, cv.astype(bool), er, res
         return sigma, e, sw, cv.astype(bool)
+
+    def noise_inverse(self, precision: int = 1) -> np.ndarray:
+        """NoiseModel::inverse (0, float) / inverse_double (1): [B][m][m] complex128."""
+        out = np.zeros((self.bins, self.m, self.m), np.complex128)
+        _capi.check(self.L.sslg_noise_inverse(self.h, int(precision), f64p(out)))
+        return out
 
     def spectrum(self, e: np.ndarray):
         e = c128(e)
@@ -503,6 +519,23 @@ class Engine:
         return idx, pw, low.astype(bool), cnt
 
 
+def _blocks_result(rc: int, n: int, blocks, idx, pw, low, power):
+    """Per-block results of a push.  On an error the blocks emitted before
+    it (the frames before the first non-finite one) travel with the
+    exception as `.partial`, so run_locate can sink them first like the
+    reference's per-frame loop."""
+    out = dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
+               count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
+               low=low[:n].astype(bool), power=None if power is None else power[:n])
+    if rc != _capi.SSLG_OK:
+        try:
+            _capi.check(rc)
+        except Exception as exc:
+            exc.partial = out
+            raise
+    return out
+
+
 def _key(a: np.ndarray):
     return (a.shape, hash(a.tobytes()))
 
@@ -511,12 +544,16 @@ _ctx_cache: Dict[tuple, Engine] = {}
 
 
 def _engine(m: int, bins: int, music: Optional[MusicConfig] = None, solver: Optional[SolverConfig] = None,
-            max_batch: int = 8) -> Engine:
+            max_batch: int = 8, purpose: str = "gsvd") -> Engine:
+    """A cached device context per configuration and purpose (the
+    peak-search context holds placeholder steering vectors, so it never
+    serves a spectrum call)."""
     music = music or MusicConfig()
     solver = solver or SolverConfig()
-    key = (m, bins, music.num_sources, float(music.denominator_floor), bool(music.squared_denominator),
+    key = (purpose, m, bins, music.num_sources, float(music.denominator_floor), bool(music.squared_denominator),
            float(music.low_power_ratio), solver.pivoting, bool(solver.canonical_subspaces),
-           bool(solver.refine_leading), bool(solver.precondition), max_batch)
+           bool(solver.refine_leading), bool(solver.precondition), int(solver.max_qr_sweeps),
+           float(solver.tolerance_scale), bool(solver.compute_residual), max_batch)
     eng = _ctx_cache.get(key)
     if eng is None:
         eng = Engine(m, bins, window_frames=1, music=music, solver=solver, max_batch=max_batch)
@@ -583,16 +620,27 @@ def gsvd_reference(noise: NoiseModel, r: CorrelationSet, cfg: Optional[SolverCon
     cfg = cfg or SolverConfig()
     cfg.validate()
     _check_batch_inputs(noise, r)
+    return _gsvd(noise, r, cfg, budget=False)
+
+
+def _gsvd(noise: NoiseModel, r: CorrelationSet, cfg: SolverConfig, budget: bool) -> GsvdBatch:
+    if not budget and cfg.max_qr_sweeps:  # gsvd_reference has no QR budget (gsvd.cpp:832-844)
+        cfg = SolverConfig(**{**cfg.__dict__, "max_qr_sweeps": 0})
     eng = _engine(r.m, r.bin_count(), solver=cfg)
     _bind_noise(eng, noise)
-    sigma, e, sw, cv = eng.gsvd(r.bins)
-    return GsvdBatch(sigma[0], e[0], sw[0], cv[0])
+    sigma, e, sw, cv, er, res = eng.gsvd(r.bins, want_er=True, want_resid=True)
+    return GsvdBatch(sigma[0], e[0], sw[0], cv[0], er[0], res[0])
 
 
 def gsvd(noise: NoiseModel, r: CorrelationSet, cfg: Optional[SolverConfig] = None, threads: int = 0) -> GsvdBatch:
-    """gsvd (gsvd.cpp:810-830): the float-typed batch result."""
-    b = gsvd_reference(noise, r, cfg, threads)
-    return GsvdBatch(b.singular_values.astype(np.float32), b.e.astype(np.complex64), b.iterations, b.converged)
+    """gsvd (gsvd.cpp:810-830): the float-typed batch result; a bin over the
+    max_qr_sweeps budget keeps converged = False (gsvd.cpp:819-827)."""
+    cfg = cfg or SolverConfig()
+    cfg.validate()
+    _check_batch_inputs(noise, r)
+    b = _gsvd(noise, r, cfg, budget=True)
+    return GsvdBatch(b.singular_values.astype(np.float32), b.e.astype(np.complex64), b.iterations, b.converged,
+                     b.e_r.astype(np.complex64), b.recon_residual.astype(np.float32))
 
 
 def calc_average_power(basis: GsvdBatch, steering: SteeringField, cfg: Optional[MusicConfig] = None,
@@ -609,7 +657,7 @@ def calc_average_power(basis: GsvdBatch, steering: SteeringField, cfg: Optional[
         raise ValidationError("num_sources must be smaller than the channel count")
     if basis.e.shape[1:] != (m, m):
         raise ValidationError("factorization channel count does not match steering field")
-    eng = _engine(m, bins, music=cfg)
+    eng = _engine(m, bins, music=cfg, purpose="spectrum")
     key = ("steer", _key(c64(steering.vectors)))
     if getattr(eng, "_steer_key", None) != key:
         eng.set_steering(steering.vectors, steering.directions)
@@ -665,7 +713,7 @@ def peak_search(power: np.ndarray, directions, topology: DirectionTopology,
     if power.shape[0] != dirs.shape[0] or len(topology.offsets) - 1 != power.shape[0]:
         raise ValidationError("peak_search input sizes do not match")
     d = power.shape[0]
-    eng = _engine(max(cfg.num_sources + 1, 2), 1, music=cfg)
+    eng = _engine(max(cfg.num_sources + 1, 2), 1, music=cfg, purpose="peaks")
     key = ("topo", d, hash(topology.offsets.tobytes()), hash(topology.nbr.tobytes()))
     if getattr(eng, "_topo_key", None) != key:
         dummy = np.zeros((d, 1, eng.m), np.complex64)
@@ -748,19 +796,28 @@ def run_locate(frames: np.ndarray, window_frames: int, noise: NoiseModel, steeri
         eng.set_noise_model(noise.k.bins)
         topo = topology or DirectionTopology.build(steering.directions)
         eng.set_steering(steering.vectors, steering.directions, topo)
-        out = eng.push(frames)
         dirs = _dirs_array(steering.directions)
-        for b in range(out["n"]):
-            ests = []
-            for i in range(int(out["count"][b])):
-                j = int(out["idx"][b, i])
-                ests.append(SourceEstimate(j, Direction(*dirs[j]), float(out["power_est"][b, i]),
-                                           bool(out["low"][b, i])))
-            if sink:
-                sink(FrameEstimates(first_frame_index + int(out["frame_index"][b]), ests))
-        return int(out["n"])
+        try:
+            out = eng.push(frames)
+        except Exception as exc:  # blocks before the failing frame reach the sink first
+            _sink_blocks(getattr(exc, "partial", None), dirs, sink, first_frame_index)
+            raise
+        return _sink_blocks(out, dirs, sink, first_frame_index)
     finally:
         eng.close()
+
+
+def _sink_blocks(out, dirs, sink, first_frame_index: int = 0) -> int:
+    if out is None:
+        return 0
+    for b in range(out["n"]):
+        ests = []
+        for i in range(int(out["count"][b])):
+            j = int(out["idx"][b, i])
+            ests.append(SourceEstimate(j, Direction(*dirs[j]), float(out["power_est"][b, i]), bool(out["low"][b, i])))
+        if sink:
+            sink(FrameEstimates(first_frame_index + int(out["frame_index"][b]), ests))
+    return int(out["n"])
 
 
 def run_locate_samples(audio: np.ndarray, stft: StftConfig, window_frames: int, noise: NoiseModel,
@@ -789,16 +846,12 @@ def run_locate_samples(audio: np.ndarray, stft: StftConfig, window_frames: int, 
         topo = topology or DirectionTopology.build(steering.directions)
         eng.set_steering(steering.vectors, steering.directions, topo)
         eng.set_stft(stft)
-        out = eng.locate_samples(audio)
         dirs = _dirs_array(steering.directions)
-        for b in range(out["n"]):
-            ests = []
-            for i in range(int(out["count"][b])):
-                j = int(out["idx"][b, i])
-                ests.append(SourceEstimate(j, Direction(*dirs[j]), float(out["power_est"][b, i]),
-                                           bool(out["low"][b, i])))
-            if sink:
-                sink(FrameEstimates(int(out["frame_index"][b]), ests))
-        return int(out["n"])
+        try:
+            out = eng.locate_samples(audio)
+        except Exception as exc:
+            _sink_blocks(getattr(exc, "partial", None), dirs, sink)
+            raise
+        return _sink_blocks(out, dirs, sink)
     finally:
         eng.close()

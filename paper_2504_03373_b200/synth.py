@@ -128,7 +128,9 @@ def drone_scene(name: str = "c3", m: int = 60, geometry: str = "circular", radiu
 CONFIGS = {
     # BASELINE.json configs[0..4]
     "c1": dict(m=8, radius=0.05, targets_deg=(40.0, 150.0), target_db=0.0, rotors_deg=(), diffuse_db=-20.0, ns=2),
-    "c2": dict(m=16, radius=0.05, targets_deg=(75.0, 200.0), target_db=0.0, rotors_deg=(300.0,), ns=2),
+    # C2: K from random_noise_model(16, 257, seed) as bench.cpp:178-206
+    "c2": dict(m=16, radius=0.05, targets_deg=(75.0, 200.0), target_db=0.0, rotors_deg=(300.0,), ns=2,
+               noise_model="random"),
     # targets at 0 dB each under four rotors at -10 dB each (-4 dB total) and a
     # -20 dB diffuse floor: ~ +4 dB per target against the whole noise field
     "c3": dict(m=60, radius=0.3, ns=2, target_db=0.0, rotor_db=-10.0),
@@ -138,9 +140,13 @@ CONFIGS = {
 
 def make(config: str, frames: int = 400, seed: int = 11) -> Workload:
     kw = dict(CONFIGS[config])
+    random_k = kw.pop("noise_model", "captured") == "random"
     if config == "c4":
         kw["dirs"] = azel_grid(5.0)
-    return drone_scene(name=config, frames=frames, seed=seed, **kw)
+    w = drone_scene(name=config, frames=frames, seed=seed, **kw)
+    if random_k:
+        w.k = random_noise_model(w.m, w.bins, seed)
+    return w
 
 
 # ---------------------------------------------------------------------------
@@ -229,6 +235,134 @@ def drone_scene_pcm(name: str = "c3", m: int = 60, radius: float = 0.3, bin_min:
 def make_pcm(config: str, duration_s: float = 2.0, seed: int = 11) -> PcmWorkload:
     kw = dict(CONFIGS[config])
     kw.pop("geometry", None)
+    random_k = kw.pop("noise_model", "captured") == "random"
     if config == "c4":
         kw["dirs"] = azel_grid(5.0)
-    return drone_scene_pcm(name=config, duration_s=duration_s, seed=seed, **kw)
+    w = drone_scene_pcm(name=config, duration_s=duration_s, seed=seed, **kw)
+    if random_k:
+        w.k = random_noise_model(w.m, w.bins, seed)
+    return w
+
+
+def describe(config: str) -> str:
+    """One-line description of a bench scene (the JSON line's workload)."""
+    kw = CONFIGS[config]
+    m, r = kw["m"], kw["radius"]
+    tg = kw.get("targets_deg", (40.0, 150.0))
+    rot = kw.get("rotors_deg", (45.0, 135.0, 225.0, 315.0))
+    tdb = kw.get("target_db", -3.0)
+    rdb = kw.get("rotor_db", 0.0)
+    dif = kw.get("diffuse_db", -20.0)
+    grid = "72 az x 19 el (1368 directions)" if config == "c4" else "72 azimuths"
+    srcs = f"{len(tg)} targets at {'/'.join(f'{a:g}' for a in tg)} deg ({tdb:g} dB)"
+    if rot:
+        srcs += f" + {len(rot)} rotor noise source(s) at {'/'.join(f'{a:g}' for a in rot)} deg ({rdb:g} dB)"
+    srcs += f" + diffuse ({dif:g} dB)"
+    k = ("K = random_noise_model(m, 257, seed) (bench.cpp:178-186)" if kw.get("noise_model") == "random"
+         else "K captured from a separate noise-only recording")
+    return (f"{m}-ch circular r={r:g} m, 16 kHz, 512-pt FFT, 257 bins, {grid}, {srcs}, {k}, "
+            f"T=50, Ns={kw['ns']}")
+
+
+# ---------------------------------------------------------------------------
+# random_noise_model (BASELINE configs[1], "C2": GSVD-MUSIC with synthetic K)
+# ---------------------------------------------------------------------------
+
+_M64 = (1 << 64) - 1
+
+
+class _MT19937_64:
+    """std::mt19937_64 (its output sequence is pinned by the C++ standard;
+    the reference draws every synthetic value from it, rng.hpp:1-34)."""
+
+    def __init__(self, seed: int):
+        mt = [0] * 312
+        mt[0] = seed & _M64
+        for i in range(1, 312):
+            mt[i] = (6364136223846793005 * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i) & _M64
+        self.mt = np.array(mt, np.uint64)
+        self.buf = None
+        self.pos = 312
+
+    def _twist(self):
+        mt = self.mt
+        um, lm = np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
+        a = np.uint64(0xB5026F5AA96619E9)
+        one = np.uint64(1)
+        for i in range(312):  # sequential dependence on updated words
+            x = (mt[i] & um) | (mt[(i + 1) % 312] & lm)
+            xa = x >> one
+            if x & one:
+                xa ^= a
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        y = mt.copy()
+        y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        y ^= y >> np.uint64(43)
+        self.buf = [int(v) for v in y]
+        self.pos = 0
+
+    def __call__(self) -> int:
+        if self.pos >= 312:
+            self._twist()
+        v = self.buf[self.pos]
+        self.pos += 1
+        return v
+
+
+def mix_seed(base: int, tag: int) -> int:
+    """ssl::mix_seed (rng.hpp:17-24)."""
+    x = (base ^ ((0x632BE59BD9B4E019 * (tag + 1)) & _M64)) & _M64
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    z = x
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _gaussian(g: _MT19937_64) -> float:
+    """ssl::gaussian (rng.hpp:27-33): Box-Muller on two 53-bit uniforms,
+    through the C library's log/cos like the reference."""
+    import math
+
+    u1 = 1.0 - float(g() >> 11) * 2.0 ** -53
+    u2 = float(g() >> 11) * 2.0 ** -53
+    return math.sqrt(-2.0 * math.log(u1)) * math.cos(2.0 * math.pi * u2)
+
+
+def random_psd(m: int, g: _MT19937_64, ridge: float) -> np.ndarray:
+    """random_psd (bench.cpp:161-176): A A^H / m in FP64 with the reference
+    matmul's k-ascending accumulation (mat.hpp:31-44), narrowed to FP32, plus
+    `ridge` on the diagonal in float, then the lower triangle mirrored."""
+    ar = np.empty((m, m))
+    ai = np.empty((m, m))
+    for i in range(m):
+        for j in range(m):
+            # cdouble(gaussian(rng), gaussian(rng)): GCC evaluates the two
+            # constructor arguments right to left, so the imaginary part draws first
+            ai[i, j] = _gaussian(g)
+            ar[i, j] = _gaussian(g)
+    # p(i, j) = sum_k a(i, k) * conj(a(j, k)), k ascending; skip exact zeros
+    pr = np.zeros((m, m))
+    pi = np.zeros((m, m))
+    for k in range(m):
+        xr, xi = ar[:, k][:, None], ai[:, k][:, None]  # a(i, k)
+        yr, yi = ar[:, k][None, :], -ai[:, k][None, :]  # conj(a(j, k)) = b(k, j)
+        nz = (xr != 0) | (xi != 0)
+        pr = np.where(nz, pr + (xr * yr - xi * yi), pr)
+        pi = np.where(nz, pi + (xr * yi + xi * yr), pi)
+    inv = 1.0 / float(m)
+    out = ((pr * inv).astype(np.float32) + 1j * (pi * inv).astype(np.float32)).astype(np.complex64)
+    d = np.arange(m)
+    out[d, d] = (out[d, d].real + np.float32(ridge)) + 1j * out[d, d].imag
+    iu = np.triu_indices(m, 1)
+    out[iu[1], iu[0]] = np.conj(out[iu])
+    return out
+
+
+def random_noise_model(m: int, bins: int, seed: int) -> np.ndarray:
+    """random_noise_model (bench.cpp:178-186): K [bins][m][m] cf32, every bin
+    Hermitian positive definite (ridge 0.5), one mt19937_64 stream per bin
+    seeded mix_seed(seed, 0x4b00 + b)."""
+    return np.stack([random_psd(m, _MT19937_64(mix_seed(seed, 0x4B00 + b)), 0.5) for b in range(bins)])

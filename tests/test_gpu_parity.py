@@ -311,18 +311,31 @@ def test_indefinite_noise_model_rejected():
         eng.set_noise_model(k, check_pd=True)
 
 
-def test_non_finite_frame_rejected_without_state_change(golden):
+def test_non_finite_frame_rejected_frame_by_frame(golden):
+    """CorrelationWindow::push rejects the non-finite frame itself
+    (correlation.cpp:16-17): the frames pushed before it stay in the window
+    and their blocks are emitted, the bad frame leaves no trace, and the
+    stream continues with the next frame."""
     from paper_2504_03373_b200 import ssl
 
     g = golden("c1_band")
-    eng = engine_for(g)
-    x = g["x"].copy()
-    bad = x[:3].copy()
-    bad[1, 0, 0] = np.nan
-    with pytest.raises(ssl.ValidationError):
-        eng.push(bad)
-    out = eng.push(x, want_power=True)  # the failed push left the window untouched
-    assert np.max(np.abs(out["power"] - g["power"]) / g["power"]) <= PBAR_TOL
+    t = int(g["t"])
+    x = g["x"]
+    k = t + 2  # bad frame after three emitted blocks
+    bad = x.copy()
+    bad[k, 3, 5] = np.nan
+    eng = engine_for(g, max_batch=32)
+    with pytest.raises(ssl.ValidationError, match="non-finite") as exc:
+        eng.push(bad[: k + 3])
+    part = exc.value.partial
+    assert part["n"] == k - t + 1
+    rest = eng.push(bad[k + 1:], want_power=True)
+    clean = engine_for(g, max_batch=32)
+    want = clean.push(np.concatenate([x[:k], x[k + 1:]]), want_power=True)
+    assert np.array_equal(np.concatenate([part["idx"], rest["idx"]]), want["idx"])
+    assert np.array_equal(rest["power"], want["power"][part["n"]:])
+    eng.close()
+    clean.close()
 
 
 def test_underfilled_window_emits_nothing(golden):

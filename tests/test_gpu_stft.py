@@ -163,6 +163,7 @@ def test_async_pushes_match_the_synchronous_stream():
     want = ref.push(frames, want_power=True)
     ref.close()
     eng = _engine(audio.shape[0], stft)
+    eng.set_async_power(True)
     tickets = [eng.push_samples_async(audio[:, a:a + 700]) for a in range(0, audio.shape[1], 700)]
     got = eng.wait_results(tickets[-1], want_power=True)
     assert got["n"] == want["n"]
