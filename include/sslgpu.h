@@ -272,6 +272,48 @@ int sslg_spectrum(sslg_ctx* ctx, const double* e, uint32_t nsets, double* power,
 int sslg_peaks(sslg_ctx* ctx, const double* power, uint32_t nsets, uint32_t* est_idx, double* est_power,
                uint8_t* est_low, uint32_t* count);
 
+/* ---- on-disk formats and output records ----------------
+ * File access is host I/O; what is loaded lands in the device context. */
+
+/* load_correlation (correlation.cpp:169-193): SSLC tensor file ("SSLC",
+ * u32le m, bins, T, then bins x m x m cf32 row-major).  Pass data == NULL to
+ * read the header only.  SSLG_IO on a bad magic / implausible header /
+ * truncated payload with the reference's messages. */
+int sslg_read_correlation_file(const char* path, uint32_t* m, uint32_t* bins, uint32_t* t, float* data,
+                               uint64_t cap_floats);
+/* save_correlation (correlation.cpp:148-167). */
+int sslg_write_correlation_file(const char* path, uint32_t m, uint32_t bins, uint32_t t, const float* data);
+/* NoiseModel::from_file (gsvd.cpp:729-734) into the context: the SSLC file,
+ * its positive-definiteness gate and the inverses.  *t (nullable) receives
+ * the header's frame count. */
+int sslg_load_noise_model(sslg_ctx* ctx, const char* path, uint32_t* bad_bin, uint32_t* t);
+/* load_steering (music.cpp:72-106): JSON header line + [dirs][bins][m] cf32
+ * payload.  Pass dirs_deg == h == NULL to read the header only; dirs_deg
+ * [dirs][2], h [dirs][bins][m] cf32 (cap_dirs = capacity in directions). */
+int sslg_read_steering_file(const char* path, uint32_t* m, uint32_t* bin_min, uint32_t* bin_max, uint32_t* dirs,
+                            double* dirs_deg, float* h, uint64_t cap_dirs);
+/* save_steering (music.cpp:47-70): the header as nlohmann::json dumps it. */
+int sslg_write_steering_file(const char* path, uint32_t m, uint32_t bin_min, uint32_t bin_max, uint32_t dirs,
+                             const double* dirs_deg, const float* h);
+/* load_steering into the context (plus DirectionTopology::build at 10 degrees,
+ * pipeline.cpp:222); *bin_min (nullable) receives the field's first bin. */
+int sslg_load_steering(sslg_ctx* ctx, const char* path, uint32_t* bin_min);
+/* capture_noise_model (synth.cpp:329-373) on the device from noise-only PCM
+ * pcm [m][nsamples] f32: the device STFT (bit-identical frames), K = sum_f
+ * x x^H / F accumulated in FP64 in frame order and narrowed to cf32
+ * (bit-identical to the reference's), then check_positive_definite.
+ * k_out (nullable) receives K [bins][m][m] cf32; install != 0 makes it the
+ * context's noise model (inverses built).  Needs sslg_set_stft. */
+int sslg_capture_noise_model(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, int install, float* k_out,
+                             uint32_t* nframes, uint32_t* bad_bin);
+/* One JSONL record of run_locate_to_stream (pipeline.cpp:265-286) for a
+ * block: {"estimates":[{"azimuth_deg","direction","elevation_deg",
+ * "low_power","power"},...],"frame"} laid out as nlohmann::json::dump()
+ * writes it (sorted keys, shortest round-trip doubles).  idx/power/low hold
+ * `count` estimates, dirs_deg the grid [dirs][2]; buf == NULL queries *len. */
+int sslg_format_estimates_json(uint64_t frame, uint32_t count, const uint32_t* idx, const double* dirs_deg,
+                               const double* power, const uint8_t* low, char* buf, uint64_t cap, uint64_t* len);
+
 /* ---- measurement ---------------------------------------------------------- */
 
 /* Device time (ms) of each stage of the last push, measured with CUDA events

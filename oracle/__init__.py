@@ -328,6 +328,45 @@ class _Ref:
                                           C.c_uint(threads), C.c_int(repeats), C.byref(out)))
         return out.value
 
+    def save_correlation(self, path: str, k, t: int):
+        k = np.ascontiguousarray(k, np.complex64)
+        self._chk(self.L.sslref_save_correlation(path.encode(), C.c_uint32(k.shape[1]), C.c_uint32(k.shape[0]),
+                                                 C.c_uint32(t), _p(k, _f32p)))
+
+    def load_correlation(self, path: str):
+        m, b, t = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        self._chk(self.L.sslref_load_correlation(path.encode(), C.byref(m), C.byref(b), C.byref(t), None))
+        k = np.zeros((b.value, m.value, m.value), np.complex64)
+        self._chk(self.L.sslref_load_correlation(path.encode(), C.byref(m), C.byref(b), C.byref(t), _p(k, _f32p)))
+        return k, t.value
+
+    def save_steering(self, path: str, m, bin_min, bin_max, dirs, h):
+        dirs = np.ascontiguousarray(dirs, np.float64)
+        h = np.ascontiguousarray(h, np.complex64)
+        self._chk(self.L.sslref_save_steering(path.encode(), C.c_uint32(m), C.c_uint32(bin_min), C.c_uint32(bin_max),
+                                              C.c_uint32(dirs.shape[0]), _p(dirs, _f64p), _p(h, _f32p)))
+
+    def load_steering(self, path: str):
+        m, lo, hi, nd = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        self._chk(self.L.sslref_load_steering(path.encode(), C.byref(m), C.byref(lo), C.byref(hi), C.byref(nd), None,
+                                              None))
+        dirs = np.zeros((nd.value, 2))
+        h = np.zeros((nd.value, hi.value - lo.value + 1, m.value), np.complex64)
+        self._chk(self.L.sslref_load_steering(path.encode(), C.byref(m), C.byref(lo), C.byref(hi), C.byref(nd),
+                                              _p(dirs, _f64p), _p(h, _f32p)))
+        return m.value, lo.value, hi.value, dirs, h
+
+    def format_estimates(self, frame: int, idx, dirs, power, low) -> str:
+        idx = np.ascontiguousarray(idx, np.uint32)
+        dirs = np.ascontiguousarray(dirs, np.float64)
+        power = np.ascontiguousarray(power, np.float64)
+        low = np.ascontiguousarray(low, np.uint8)
+        buf = C.create_string_buffer(1 << 16)
+        self._chk(self.L.sslref_format_estimates(C.c_uint64(frame), C.c_uint32(len(idx)), _p(idx, _u32p),
+                                                 _p(dirs, _f64p), _p(power, _f64p), _p(low, _u8p), buf,
+                                                 C.c_uint64(1 << 16)))
+        return buf.value.decode()
+
     def time_spectrum(self, k, r, h, music: MusicCfg, threads: int, repeats: int) -> float:
         """Median seconds of calc_average_power<float> on gsvd()'s factors of r."""
         k = np.ascontiguousarray(k, np.complex64)

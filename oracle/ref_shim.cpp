@@ -26,6 +26,8 @@
 #include "ssl/stft.hpp"
 #include "ssl/synth.hpp"
 
+#include <nlohmann/json.hpp>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
@@ -708,6 +710,98 @@ SHIM_API int sslref_run_locate(void* h, const sslref_scene* s, std::uint32_t t, 
                             ++e;
                         });
         *emitted = e;
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// on-disk formats through the reference's own readers and writers
+// ---------------------------------------------------------------------------
+
+SHIM_API int sslref_save_correlation(const char* path, std::uint32_t m, std::uint32_t bins, std::uint32_t t,
+                                     const float* k) {
+    return guarded([&] { ssl::save_correlation(path, set_from(k, m, bins), t); });
+}
+
+// load_correlation: header into m/bins/t, payload into k when non-null
+SHIM_API int sslref_load_correlation(const char* path, std::uint32_t* m, std::uint32_t* bins, std::uint32_t* t,
+                                     float* k) {
+    return guarded([&] {
+        std::uint32_t tt = 0;
+        const auto set = ssl::load_correlation(path, &tt);
+        *m = set.m;
+        *bins = std::uint32_t(set.bins.size());
+        *t = tt;
+        if (k) {
+            std::size_t o = 0;
+            for (const auto& mat : set.bins)
+                for (const auto& z : mat.data) {
+                    k[o++] = z.real();
+                    k[o++] = z.imag();
+                }
+        }
+    });
+}
+
+SHIM_API int sslref_save_steering(const char* path, std::uint32_t m, std::uint32_t bin_min, std::uint32_t bin_max,
+                                  std::uint32_t dirs, const double* dirs_deg, const float* h) {
+    return guarded([&] {
+        ssl::SteeringField f;
+        f.m = m;
+        f.bin_min = bin_min;
+        f.bin_max = bin_max;
+        for (std::uint32_t d = 0; d < dirs; ++d) f.directions.push_back({dirs_deg[2 * d], dirs_deg[2 * d + 1]});
+        const std::size_t n = std::size_t(dirs) * (bin_max - bin_min + 1) * m;
+        f.vectors.resize(n);
+        for (std::size_t i = 0; i < n; ++i) f.vectors[i] = ssl::cfloat(h[2 * i], h[2 * i + 1]);
+        ssl::save_steering(f, path);
+    });
+}
+
+SHIM_API int sslref_load_steering(const char* path, std::uint32_t* m, std::uint32_t* bin_min, std::uint32_t* bin_max,
+                                  std::uint32_t* dirs, double* dirs_deg, float* h) {
+    return guarded([&] {
+        const auto f = ssl::load_steering(path);
+        *m = f.m;
+        *bin_min = f.bin_min;
+        *bin_max = f.bin_max;
+        *dirs = std::uint32_t(f.directions.size());
+        if (dirs_deg)
+            for (std::size_t d = 0; d < f.directions.size(); ++d) {
+                dirs_deg[2 * d] = f.directions[d].azimuth_deg;
+                dirs_deg[2 * d + 1] = f.directions[d].elevation_deg;
+            }
+        if (h)
+            for (std::size_t i = 0; i < f.vectors.size(); ++i) {
+                h[2 * i] = f.vectors[i].real();
+                h[2 * i + 1] = f.vectors[i].imag();
+            }
+    });
+}
+
+// The JSONL record run_locate_to_stream's sink writes (pipeline.cpp:268-283),
+// built the same way with the same nlohmann::json.  Test infrastructure: the
+// checker for the engine's record formatter.
+SHIM_API int sslref_format_estimates(std::uint64_t frame, std::uint32_t count, const std::uint32_t* idx,
+                                     const double* dirs_deg, const double* power, const std::uint8_t* low,
+                                     char* buf, std::uint64_t cap) {
+    return guarded([&] {
+        nlohmann::json line;
+        line["frame"] = frame;
+        auto arr = nlohmann::json::array();
+        for (std::uint32_t i = 0; i < count; ++i) {
+            nlohmann::json e;
+            e["azimuth_deg"] = dirs_deg[2 * std::size_t(idx[i])];
+            e["elevation_deg"] = dirs_deg[2 * std::size_t(idx[i]) + 1];
+            e["power"] = power[i];
+            e["low_power"] = low[i] != 0;
+            e["direction"] = idx[i];
+            arr.push_back(std::move(e));
+        }
+        line["estimates"] = std::move(arr);
+        const std::string s = line.dump();
+        if (s.size() + 1 > cap) throw ssl::ValidationError("buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
     });
 }
 

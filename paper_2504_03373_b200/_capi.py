@@ -88,6 +88,16 @@ EXPORTS = {
     "sslg_gsvd_ex": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _f64p, _u32p, _u8p, _f64p]),
     "sslg_noise_inverse": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
     "sslg_set_async_power": (C.c_int, [C.c_void_p, C.c_int]),
+    "sslg_read_correlation_file": (C.c_int, [C.c_char_p, _u32p, _u32p, _u32p, _f32p, C.c_uint64]),
+    "sslg_write_correlation_file": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, _f32p]),
+    "sslg_load_noise_model": (C.c_int, [C.c_void_p, C.c_char_p, _u32p, _u32p]),
+    "sslg_read_steering_file": (C.c_int, [C.c_char_p, _u32p, _u32p, _u32p, _u32p, _f64p, _f32p, C.c_uint64]),
+    "sslg_write_steering_file": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _f64p,
+                                           _f32p]),
+    "sslg_load_steering": (C.c_int, [C.c_void_p, C.c_char_p, _u32p]),
+    "sslg_capture_noise_model": (C.c_int, [C.c_void_p, _f32p, C.c_uint64, C.c_int, _f32p, _u32p, _u32p]),
+    "sslg_format_estimates_json": (C.c_int, [C.c_uint64, C.c_uint32, _u32p, _f64p, _f64p, _u8p, C.c_char_p,
+                                             C.c_uint64, C.POINTER(C.c_uint64)]),
     "sslg_spectrum": (C.c_int, [C.c_void_p, _f64p, C.c_uint32, _f64p, _f64p]),
     "sslg_peaks": (C.c_int, [C.c_void_p, _f64p, C.c_uint32, _u32p, _f64p, _u8p, _u32p]),
     "sslg_last_stage_ms": (C.c_int, [C.c_void_p, _f32p]),

@@ -49,13 +49,21 @@ __global__ void transpose_sq_kernel(const double2* __restrict__ in, double2* __r
 using namespace sslg;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int set_err(int code, const std::string& msg) {
+namespace sslg {
+// the message of the last failure on this thread (sslg_last_error); shared
+// with the format loaders (formats.cu)
+int set_error(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+}  // namespace sslg
+
+namespace {
+
+int set_err(int code, const std::string& msg) { return sslg::set_error(code, msg); }
 
 #define CU(call)                                                                                   \
     do {                                                                                           \
@@ -523,6 +531,58 @@ int sslg_get_config(const sslg_ctx* c, sslg_config* cfg) {
     return SSLG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// check_positive_definite (gsvd.cpp:736-754) of a device K [bins][m][m]
+int pd_gate(sslg_ctx* c, const float2* kdev, uint32_t* bad_bin) {
+    const sslg_config& g = c->cfg;
+    TRY(reset_flags(c));
+    unsigned int fl[5];
+    double* min_eig = nullptr;
+    TRY(dalloc(&min_eig, g.bins));
+    launch_pd_check(kdev, (int)g.m, (int)g.bins, c->flags + 3, c->flags + 4, min_eig, c->stream);
+    int rc = check_last_launch("pd_check_kernel");
+    if (!rc) rc = sync_flags(c, fl, 5);
+    if (!rc && (fl[3] != 0xffffffffu || fl[4] != 0xffffffffu)) {
+        // the reference checks bin by bin, Hermitian test first (gsvd.cpp:737-752)
+        const unsigned b = std::min(fl[3], fl[4]);
+        const bool herm = fl[3] == b;
+        if (bad_bin) *bad_bin = b;
+        double ev = 0;
+        if (!herm) cudaMemcpy(&ev, min_eig + b, sizeof ev, cudaMemcpyDeviceToHost);
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "%f", ev);  // std::to_string(double)
+        rc = set_err(SSLG_NUMERICAL, herm ? "noise model is not Hermitian at bin " + std::to_string(b)
+                                          : "noise model is not positive definite at bin " + std::to_string(b) +
+                                                " (min eigenvalue " + buf + ")");
+    }
+    cudaFree(min_eig);
+    return rc;
+}
+
+// NoiseModel::prepare_inverses (gsvd.cpp:756-768) of the K already in c->k
+int install_noise(sslg_ctx* c, uint32_t* bad_bin) {
+    const sslg_config& g = c->cfg;
+    TRY(reset_flags(c));
+    unsigned int fl[5];
+    launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, c->kinv, c->flags + 1, c->flags + 2, c->stream, g.pivoting);
+    TRY(check_last_launch("gauss_jordan_kernel"));
+    TRY(sync_flags(c, fl, 3));
+    const unsigned bad = std::min(fl[1], fl[2]);
+    if (bad != 0xffffffffu) {
+        if (bad_bin) *bad_bin = bad;
+        return set_err(SSLG_NUMERICAL, "noise matrix is singular at bin " + std::to_string(bad));
+    }
+    c->have_noise = true;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* bad_bin) {
     if (!c || !k) return set_err(SSLG_VALIDATION, "null argument");
     TRY(require_no_async(c));
@@ -533,43 +593,10 @@ int sslg_set_noise_model(sslg_ctx* c, const float* k, int check_pd, uint32_t* ba
     const size_t n = g.bins * mm * 2;
     for (size_t i = 0; i < n; ++i)
         if (!std::isfinite(k[i])) return set_err(SSLG_VALIDATION, "non-finite correlation entry");
+    c->have_noise = false;
     CU(cudaMemcpyAsync(c->k, k, g.bins * mm * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
-    TRY(reset_flags(c));
-    unsigned int fl[5];
-    if (check_pd) {
-        double* min_eig = nullptr;
-        TRY(dalloc(&min_eig, g.bins));
-        launch_pd_check(c->k, (int)g.m, (int)g.bins, c->flags + 3, c->flags + 4, min_eig, c->stream);
-        int rc = check_last_launch("pd_check_kernel");
-        if (!rc) rc = sync_flags(c, fl, 5);
-        if (!rc && (fl[3] != 0xffffffffu || fl[4] != 0xffffffffu)) {
-            // the reference checks bin by bin, Hermitian test first (gsvd.cpp:737-752)
-            c->have_noise = false;
-            const unsigned b = std::min(fl[3], fl[4]);
-            const bool herm = fl[3] == b;
-            if (bad_bin) *bad_bin = b;
-            double ev = 0;
-            if (!herm) cudaMemcpy(&ev, min_eig + b, sizeof ev, cudaMemcpyDeviceToHost);
-            char buf[64];
-            std::snprintf(buf, sizeof buf, "%f", ev);  // std::to_string(double)
-            rc = set_err(SSLG_NUMERICAL, herm ? "noise model is not Hermitian at bin " + std::to_string(b)
-                                              : "noise model is not positive definite at bin " + std::to_string(b) +
-                                                    " (min eigenvalue " + buf + ")");
-        }
-        cudaFree(min_eig);
-        TRY(rc);
-    }
-    launch_gauss_jordan(c->k, (int)g.m, (int)g.bins, c->kinv, c->flags + 1, c->flags + 2, c->stream, g.pivoting);
-    TRY(check_last_launch("gauss_jordan_kernel"));
-    TRY(sync_flags(c, fl, 3));
-    const unsigned bad = std::min(fl[1], fl[2]);
-    if (bad != 0xffffffffu) {
-        c->have_noise = false;
-        if (bad_bin) *bad_bin = bad;
-        return set_err(SSLG_NUMERICAL, "noise matrix is singular at bin " + std::to_string(bad));
-    }
-    c->have_noise = true;
-    return SSLG_OK;
+    if (check_pd) TRY(pd_gate(c, c->k, bad_bin));
+    return install_noise(c, bad_bin);
 }
 
 int sslg_noise_inverse(sslg_ctx* c, int precision, double* out) {
@@ -1223,6 +1250,48 @@ int sslg_stft(sslg_ctx* c, const float* pcm, uint64_t nsamples, float* frames, u
         CU(cudaStreamSynchronize(c->stream));
     }
     return SSLG_OK;
+}
+
+int sslg_capture_noise_model(sslg_ctx* c, const float* pcm, uint64_t nsamples, int install, float* k_out,
+                             uint32_t* nframes, uint32_t* bad_bin) {
+    if (!c || (!pcm && nsamples)) return set_err(SSLG_VALIDATION, "null argument");
+    if (!c->have_stft) return set_err(SSLG_VALIDATION, "STFT not configured (sslg_set_stft)");
+    TRY(require_no_async(c));
+    CU(cudaSetDevice(c->cfg.device));
+    TRY(check_device_gate(c));
+    const sslg_config& g = c->cfg;
+    const size_t L = c->stft.frame_length, S = c->stft.shift;
+    const uint64_t total = nsamples < L ? 0 : (nsamples - L) / S + 1;  // stft_frame_count (stft.cpp:38-42)
+    if (nframes) *nframes = (uint32_t)total;
+    if (total == 0) return set_err(SSLG_VALIDATION, "noise capture scene is shorter than one frame");
+    const size_t mm = (size_t)g.m * g.m, n = g.bins * mm;
+    // acc: FP64 sums [bins][m][m] (e_tmp); K: cf32 (the first set of R)
+    double2* acc = c->e_tmp;
+    float2* kdev = c->r;
+    c->launches = 0;
+    CU(cudaMemsetAsync(acc, 0, n * sizeof(double2), c->stream));
+    float* stage = c->samp[c->samp_cur ^ 1];
+    for (uint64_t f0 = 0; f0 < total; f0 += g.max_batch) {
+        const int nf = (int)std::min<uint64_t>(total - f0, g.max_batch);
+        const size_t span = (size_t)(nf - 1) * S + L;
+        CU(cudaMemcpy2DAsync(stage, c->samp_cap * sizeof(float), pcm + f0 * S, nsamples * sizeof(float),
+                             span * sizeof(float), g.m, cudaMemcpyHostToDevice, c->stream));
+        TRY(launch_stft_frames(c, stage, c->samp_cap, nf, c->frame_scratch, nf, 0));
+        launch_capture_accum(c->frame_scratch, nf, (int)g.m, (int)g.bins, acc, c->stream);
+        ++c->launches;
+        TRY(check_last_launch("capture_accum_kernel"));
+    }
+    launch_capture_narrow(acc, n, 1.0 / double(total), kdev, c->stream);
+    ++c->launches;
+    TRY(check_last_launch("capture_narrow_kernel"));
+    if (k_out) CU(cudaMemcpyAsync(k_out, kdev, n * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    // capture_noise_model ends with check_positive_definite (synth.cpp:370)
+    TRY(pd_gate(c, kdev, bad_bin));
+    if (!install) return SSLG_OK;
+    c->have_noise = false;
+    CU(cudaMemcpyAsync(c->k, kdev, n * sizeof(float2), cudaMemcpyDeviceToDevice, c->stream));
+    return install_noise(c, bad_bin);
 }
 
 int sslg_samples_pending(const sslg_ctx* c, uint64_t nsamples, uint32_t* frames, uint32_t* blocks) {

@@ -104,6 +104,9 @@ struct SpecArgs {
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s);
+// capture_noise_model (synth.cpp:329-373): FP64 sums of x x^H over frames, then K = float(sum / F)
+void launch_capture_accum(const float2* frames, int nframes, int m, int bins, double2* acc, cudaStream_t s);
+void launch_capture_narrow(const double2* acc, size_t n, double inv, float2* k, cudaStream_t s);
 void launch_steering_prep(const float2* h_in, float2* h_t, double* num, int m, int bins, int dirs,
                           cudaStream_t s);
 

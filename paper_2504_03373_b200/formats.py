@@ -1,99 +1,86 @@
-"""On-disk inputs of the path: the SSLC correlation/noise-model tensor
-(correlation.cpp:133-193) and the steering-field file (music.cpp:47-106).
-Plain host I/O feeding the device engine."""
+"""On-disk inputs and output records of the path, through
+the C ABI of libsslgpu.so (include/sslgpu.h, csrc/formats.cu):
+
+  SSLC correlation / noise-model tensors  load_correlation, save_correlation
+                                          (correlation.cpp:133-193)
+  steering-field files                    load_steering, save_steering
+                                          (music.cpp:47-106)
+  JSONL estimate records                  format_estimates_json
+                                          (pipeline.cpp:265-286)
+
+Same names, argument meaning and errors (IoError / ValidationError) as the
+reference's functions."""
 from __future__ import annotations
 
-import json
-import struct
+import ctypes as C
 
 import numpy as np
 
-from .errors import IoError, ValidationError
-
-_MAGIC = b"SSLC"
+from . import _capi
+from ._capi import f32p, f64p, u8p, u32p
 
 
 def save_correlation(path: str, bins: np.ndarray, t: int) -> None:
-    """save_correlation (correlation.cpp:148-167): magic, u32 m, bins, T, then
-    row-major interleaved float32 per bin."""
+    """save_correlation (correlation.cpp:148-167)."""
     bins = np.ascontiguousarray(bins, np.complex64)
     if bins.ndim != 3 or bins.shape[1] != bins.shape[2] or bins.shape[0] == 0:
+        from .errors import ValidationError
+
         raise ValidationError("correlation matrix dimension mismatch")
-    if not np.all(np.isfinite(bins.view(np.float32))):
-        raise ValidationError("non-finite correlation entry")
-    try:
-        with open(path, "wb") as f:
-            f.write(_MAGIC)
-            f.write(struct.pack("<III", bins.shape[1], bins.shape[0], t))
-            f.write(bins.astype("<c8").tobytes())
-    except OSError as e:
-        raise IoError(f"cannot open {path} for writing") from e
+    _capi.check(_capi.load().sslg_write_correlation_file(path.encode(), bins.shape[1], bins.shape[0], int(t),
+                                                         f32p(bins)))
 
 
 def load_correlation(path: str):
     """load_correlation (correlation.cpp:169-193) -> (CorrelationSet, T)."""
     from .ssl import CorrelationSet
 
-    try:
-        with open(path, "rb") as f:
-            data = f.read()
-    except OSError as e:
-        raise IoError("cannot open " + path) from e
-    if len(data) < 4 or data[:4] != _MAGIC:
-        raise IoError(path + ": not a correlation tensor file")
-    if len(data) < 16:
-        raise IoError(path + ": implausible header")
-    m, nb, t = struct.unpack("<III", data[4:16])
-    if m < 1 or m > 4096 or nb < 1 or nb > (1 << 20):
-        raise IoError(path + ": implausible header")
-    need = nb * m * m * 8
-    if len(data) - 16 < need:
-        raise IoError(path + ": truncated payload")
-    arr = np.frombuffer(data[16:16 + need], "<c8").astype(np.complex64).reshape(nb, m, m)
-    s = CorrelationSet(m, arr.copy())
-    s.validate()
-    return s, t
+    L = _capi.load()
+    m, nb, t = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _capi.check(L.sslg_read_correlation_file(path.encode(), C.byref(m), C.byref(nb), C.byref(t), None, 0))
+    arr = np.zeros((nb.value, m.value, m.value), np.complex64)
+    _capi.check(L.sslg_read_correlation_file(path.encode(), None, None, None, f32p(arr), arr.size * 2))
+    return CorrelationSet(m.value, arr), t.value
 
 
 def save_steering(path: str, field) -> None:
-    """save_steering (music.cpp:47-70): one JSON header line then float32 pairs."""
+    """save_steering (music.cpp:47-70): one JSON header line, then float32 pairs."""
     field.validate()
-    header = {"bin_max": int(field.bin_max), "bin_min": int(field.bin_min),
-              "directions": [[float(a), float(e)] for a, e in np.asarray(field.directions).reshape(-1, 2)],
-              "m": int(field.m)}
-    try:
-        with open(path, "wb") as f:
-            f.write(json.dumps(header, separators=(",", ":")).encode() + b"\n")
-            f.write(np.ascontiguousarray(field.vectors, np.complex64).astype("<c8").tobytes())
-    except OSError as e:
-        raise IoError(f"cannot open {path} for writing") from e
+    dirs = np.ascontiguousarray(np.asarray(field.directions, np.float64).reshape(-1, 2))
+    vec = np.ascontiguousarray(field.vectors, np.complex64)
+    _capi.check(_capi.load().sslg_write_steering_file(path.encode(), field.m, field.bin_min, field.bin_max,
+                                                      dirs.shape[0], f64p(dirs), f32p(vec)))
 
 
 def load_steering(path: str):
     """load_steering (music.cpp:72-106)."""
     from .ssl import SteeringField
 
-    try:
-        with open(path, "rb") as f:
-            data = f.read()
-    except OSError as e:
-        raise IoError("cannot open " + path) from e
-    nl = data.find(b"\n")
-    if nl < 0:
-        raise IoError("missing header line in " + path)
-    try:
-        h = json.loads(data[:nl])
-        m, bmin, bmax = int(h["m"]), int(h["bin_min"]), int(h["bin_max"])
-        dirs = np.array([[float(d[0]), float(d[1])] for d in h["directions"]], np.float64).reshape(-1, 2)
-    except (ValueError, KeyError, TypeError, IndexError) as e:
-        raise IoError(f"bad steering header in {path}: {e}") from e
-    if m == 0 or bmax < bmin or len(dirs) == 0:
-        raise IoError("bad steering header in " + path)
-    count = len(dirs) * (bmax - bmin + 1) * m
-    payload = data[nl + 1:]
-    if len(payload) < count * 8:
-        raise IoError("truncated steering payload in " + path)
-    vec = np.frombuffer(payload[: count * 8], "<c8").astype(np.complex64).reshape(len(dirs), bmax - bmin + 1, m)
-    f = SteeringField(m, bmin, bmax, dirs, vec.copy())
+    L = _capi.load()
+    m, lo, hi, nd = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+    _capi.check(L.sslg_read_steering_file(path.encode(), C.byref(m), C.byref(lo), C.byref(hi), C.byref(nd), None,
+                                          None, 0))
+    dirs = np.zeros((nd.value, 2), np.float64)
+    vec = np.zeros((nd.value, hi.value - lo.value + 1, m.value), np.complex64)
+    _capi.check(L.sslg_read_steering_file(path.encode(), None, None, None, None, f64p(dirs), f32p(vec), nd.value))
+    f = SteeringField(m.value, lo.value, hi.value, dirs, vec)
     f.validate()
     return f
+
+
+def format_estimates_json(frame_index: int, estimates, directions) -> str:
+    """The JSON line run_locate_to_stream writes for one FrameEstimates
+    (pipeline.cpp:268-283), as nlohmann::json::dump() lays it out."""
+    dirs = np.ascontiguousarray(np.asarray(directions, np.float64).reshape(-1, 2))
+    n = len(estimates)
+    idx = np.array([e.direction_index for e in estimates], np.uint32)
+    pw = np.array([e.power for e in estimates], np.float64)
+    low = np.array([1 if e.low_power else 0 for e in estimates], np.uint8)
+    L = _capi.load()
+    ln = C.c_uint64()
+    _capi.check(L.sslg_format_estimates_json(int(frame_index), n, u32p(idx), f64p(dirs), f64p(pw), u8p(low), None, 0,
+                                             C.byref(ln)))
+    buf = C.create_string_buffer(ln.value + 1)
+    _capi.check(L.sslg_format_estimates_json(int(frame_index), n, u32p(idx), f64p(dirs), f64p(pw), u8p(low), buf,
+                                             ln.value + 1, C.byref(ln)))
+    return buf.value.decode()

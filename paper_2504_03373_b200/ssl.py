@@ -489,6 +489,37 @@ class Engine:
             return sigma, e, sw, cv.astype(bool), er, res
         return sigma, e, sw, cv.astype(bool)
 
+    def load_noise_model(self, path: str) -> int:
+        """NoiseModel::from_file (gsvd.cpp:729-734) into this context; returns T."""
+        bad, t = C.c_uint32(), C.c_uint32()
+        _capi.check(self.L.sslg_load_noise_model(self.h, path.encode(), C.byref(bad), C.byref(t)))
+        self._noise_key = ("file", path)
+        return t.value
+
+    def load_steering(self, path: str) -> int:
+        """load_steering (music.cpp:72-106) into this context; returns bin_min."""
+        lo = C.c_uint32()
+        _capi.check(self.L.sslg_load_steering(self.h, path.encode(), C.byref(lo)))
+        cfg = _capi.Config()
+        _capi.check(self.L.sslg_get_config(self.h, C.byref(cfg)))
+        self.dirs = cfg.dirs
+        return lo.value
+
+    def capture_noise_model(self, pcm: np.ndarray, install: bool = True) -> np.ndarray:
+        """capture_noise_model (synth.cpp:329-373) on the device from
+        noise-only PCM [m][n]: K [bins][m][m] complex64 (PD-gated); installed
+        as this context's noise model unless install=False."""
+        pcm = np.ascontiguousarray(pcm, np.float32)
+        if pcm.ndim != 2 or pcm.shape[0] != self.m:
+            raise ValidationError("sample block channel count does not match the engine")
+        k = np.zeros((self.bins, self.m, self.m), np.complex64)
+        nf, bad = C.c_uint32(), C.c_uint32()
+        _capi.check(self.L.sslg_capture_noise_model(self.h, f32p(pcm), pcm.shape[1], int(install), f32p(k),
+                                                    C.byref(nf), C.byref(bad)))
+        if install:
+            self._noise_key = _key(k)
+        return k
+
     def noise_inverse(self, precision: int = 1) -> np.ndarray:
         """NoiseModel::inverse (0, float) / inverse_double (1): [B][m][m] complex128."""
         out = np.zeros((self.bins, self.m, self.m), np.complex128)
@@ -567,6 +598,8 @@ def _engine(m: int, bins: int, music: Optional[MusicConfig] = None, solver: Opti
 
 
 class NoiseModel:
+    """ssl::NoiseModel (gsvd.hpp:31-50); the inverses live in device contexts."""
+
     def __init__(self, k: CorrelationSet):
         self.k = k
         self._prepared: Optional[str] = None
@@ -584,6 +617,21 @@ class NoiseModel:
         n = NoiseModel(load_correlation(path)[0])
         n.check_positive_definite()
         return n
+
+    @staticmethod
+    def capture(audio: np.ndarray, stft: "StftConfig") -> "NoiseModel":
+        """capture_noise_model (synth.cpp:329-373) from a noise-only
+        SampleBlock audio [m][n]: device STFT + FP64 frame sums, bit-identical
+        to the reference's K, PD-gated."""
+        audio = np.ascontiguousarray(audio, np.float32)
+        stft.validate()
+        eng = Engine(audio.shape[0], stft.bin_count(), window_frames=1, max_batch=16)
+        try:
+            eng.set_stft(stft)
+            k = eng.capture_noise_model(audio, install=False)
+        finally:
+            eng.close()
+        return NoiseModel(CorrelationSet(audio.shape[0], k))
 
     def check_positive_definite(self) -> None:
         """Throws NumericalError unless every bin is Hermitian PD (device)."""
