@@ -242,6 +242,11 @@ int sslg_wait_results(sslg_ctx* ctx, uint64_t ticket, uint32_t cap_blocks, sslg_
  * frames; r_out [emitted][bins][m][m] cf32 bit-identical to the reference. */
 int sslg_correlation(sslg_ctx* ctx, const float* x, uint32_t nframes, float* r_out, uint32_t* emitted);
 
+/* The newest correlation set the window produced (by sslg_correlation or a
+ * push): r_out [bins][m][m] cf32 -- CorrelationWindow::normalized
+ * (correlation.cpp:112-130).  SSLG_VALIDATION while the window is underfilled. */
+int sslg_last_correlation(sslg_ctx* ctx, float* r_out);
+
 /* gsvd / gsvd_reference batch drivers (gsvd.hpp:160-163) for nsets
  * correlation sets r [nsets][bins][m][m]: sigma [nsets][bins][m] descending,
  * e [nsets][bins][m][m] (row-major, column j = vector j), sweeps / conv

@@ -85,6 +85,7 @@ EXPORTS = {
     "sslg_synchronize": (C.c_int, [C.c_void_p]),
     "sslg_correlation": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f32p, _u32p]),
     "sslg_gsvd": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _u32p, _u8p]),
+    "sslg_last_correlation": (C.c_int, [C.c_void_p, _f32p]),
     "sslg_gsvd_ex": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _f64p, _u32p, _u8p, _f64p]),
     "sslg_noise_inverse": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
     "sslg_set_async_power": (C.c_int, [C.c_void_p, C.c_int]),

@@ -162,6 +162,8 @@ struct sslg_ctx {
     bool poisoned = false;
     uint32_t poison_code = 0;
     bool async_power = false;   // async pushes also copy back power [e][dirs] (sslg_set_async_power)
+    bool slots_ready = false;   // pinned result ring allocated (ensure_slots)
+    int last_corr = -1;         // index in r of the newest set emitted by sslg_correlation (-1: none)
     // device-frame pushes (sslg_push_frames_device) gate on the device through
     // the same abort word; their window counters are kept until the next
     // synchronizing call verifies the word (check_device_gate)
@@ -320,6 +322,7 @@ int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
     }
     c->last_first_frame = c->pushed - n;
     c->last_emitted = (uint32_t)n;
+    if (n > 0) c->last_corr = n - 1;
     if (n > 0) {
         TRY(run_gsvd(c, n));
         TRY(run_music(c, n));
@@ -377,6 +380,23 @@ int require_ready(sslg_ctx* c, bool verify_device_gate = true) {
     TRY(require_no_async(c));
     CU(cudaSetDevice(c->cfg.device));
     if (verify_device_gate || c->dev_unverified.size() >= 1024) TRY(check_device_gate(c));
+    return 0;
+}
+
+// The pinned result ring of sslg_push_samples_async, allocated on first use.
+int ensure_slots(sslg_ctx* c) {
+    if (c->slots_ready) return 0;
+    const size_t NB = c->cfg.max_batch, ns = c->cfg.num_sources;
+    for (auto& sl : c->slots) {
+        if (cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess ||
+            cudaMallocHost(&sl.idx, NB * ns * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMallocHost(&sl.pw, NB * ns * sizeof(double)) != cudaSuccess ||
+            cudaMallocHost(&sl.low, NB * ns) != cudaSuccess ||
+            cudaMallocHost(&sl.cnt, NB * sizeof(uint32_t)) != cudaSuccess ||
+            (c->dirs && cudaMallocHost(&sl.power, NB * c->dirs * sizeof(double)) != cudaSuccess))
+            return set_err(SSLG_DEVICE, "pinned result ring allocation failed");  // sslg_destroy frees the rest
+    }
+    c->slots_ready = true;
     return 0;
 }
 
@@ -479,15 +499,8 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     rc |= dalloc(&c->abort, 1);
     if (!rc && cudaMemsetAsync(c->abort, 0, sizeof(unsigned int), c->stream) != cudaSuccess)
         rc = set_err(SSLG_DEVICE, "cudaMemset failed");
-    for (auto& sl : c->slots) {
-        if (rc) break;
-        if (cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess ||
-            cudaMallocHost(&sl.idx, NB * g.num_sources * sizeof(uint32_t)) != cudaSuccess ||
-            cudaMallocHost(&sl.pw, NB * g.num_sources * sizeof(double)) != cudaSuccess ||
-            cudaMallocHost(&sl.low, NB * g.num_sources) != cudaSuccess ||
-            cudaMallocHost(&sl.cnt, NB * sizeof(uint32_t)) != cudaSuccess)
-            rc = set_err(SSLG_DEVICE, "pinned result ring allocation failed");
-    }
+    // the pinned result ring of the asynchronous path is allocated on its
+    // first use (ensure_slots): most contexts never need its 80 pinned buffers
     for (int i = 0; i < 6 && !rc; ++i)
         if (cudaEventCreate(&c->ev[i]) != cudaSuccess) rc = set_err(SSLG_DEVICE, "cudaEventCreate failed");
     if (!rc && cudaMemsetAsync(c->state, 0, B * mm * sizeof(double2), c->stream) != cudaSuccess)
@@ -719,7 +732,7 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
         rc |= dalloc(&est_idx, NB * g.num_sources);
         rc |= dalloc(&est_pw, NB * g.num_sources);
         rc |= dalloc(&est_low, NB * g.num_sources);
-        for (int i = 0; i < sslg_ctx::kSlots && !rc; ++i)
+        for (int i = 0; i < sslg_ctx::kSlots && !rc && c->slots_ready; ++i)
             if (cudaMallocHost(&slot_power[i], NB * dirs * sizeof(double)) != cudaSuccess)
                 rc = set_err(SSLG_DEVICE, "pinned result ring allocation failed");
         if (rc) {
@@ -742,7 +755,7 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
         c->est_idx = est_idx;
         c->est_pw = est_pw;
         c->est_low = est_low;
-        for (int i = 0; i < sslg_ctx::kSlots; ++i) {
+        for (int i = 0; i < sslg_ctx::kSlots && c->slots_ready; ++i) {
             if (c->slots[i].power) cudaFreeHost(c->slots[i].power);
             c->slots[i].power = slot_power[i];
         }
@@ -772,6 +785,7 @@ int sslg_reset_window(sslg_ctx* c) {
     c->pushed = 0;
     c->since = 0;
     c->last_emitted = 0;
+    c->last_corr = -1;
     c->samp_fill = 0;
     // asynchronous pushes in flight are discarded
     CU(cudaMemsetAsync(c->abort, 0, sizeof(unsigned int), c->stream));
@@ -921,6 +935,7 @@ int sslg_correlation(sslg_ctx* c, const float* x, uint32_t nframes, float* r_out
             ++c->pushed;
             if (++c->since >= (long long)g.rebuild_interval) c->since = 0;
         }
+        if (n > 0) c->last_corr = n - 1;
         if (n > 0 && r_out)
             CU(cudaMemcpyAsync(r_out + out * rsz * 2, c->r, n * rsz * sizeof(float2), cudaMemcpyDeviceToHost,
                                c->stream));
@@ -930,6 +945,17 @@ int sslg_correlation(sslg_ctx* c, const float* x, uint32_t nframes, float* r_out
         if (emitted) *emitted = out;
         if (bad) return set_err(SSLG_VALIDATION, "non-finite spectrum value (frame " + std::to_string(done) + ")");
     }
+    return SSLG_OK;
+}
+
+int sslg_last_correlation(sslg_ctx* c, float* r_out) {
+    if (!c || !r_out) return set_err(SSLG_VALIDATION, "null argument");
+    if (c->last_corr < 0) return set_err(SSLG_VALIDATION, "correlation window underfilled");
+    CU(cudaSetDevice(c->cfg.device));
+    const size_t rsz = (size_t)c->cfg.bins * c->cfg.m * c->cfg.m;
+    CU(cudaMemcpyAsync(r_out, c->r + (size_t)c->last_corr * rsz, rsz * sizeof(float2), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CU(cudaStreamSynchronize(c->stream));
     return SSLG_OK;
 }
 
@@ -950,6 +976,7 @@ int sslg_gsvd_ex(sslg_ctx* c, const float* r, uint32_t nsets, double* sigma, dou
     for (size_t i = 0; i < (size_t)nsets * B * mm * 2; ++i)
         if (!std::isfinite(r[i])) return set_err(SSLG_VALIDATION, "non-finite correlation entry");
     c->launches = 0;
+    c->last_corr = -1;  // c->r now holds the caller's sets
     const bool want_resid = resid && g.compute_residual;
     std::vector<uint32_t> sw_tmp;
     for (uint32_t done = 0; done < nsets;) {
@@ -1268,6 +1295,7 @@ int sslg_capture_noise_model(sslg_ctx* c, const float* pcm, uint64_t nsamples, i
     // acc: FP64 sums [bins][m][m] (e_tmp); K: cf32 (the first set of R)
     double2* acc = c->e_tmp;
     float2* kdev = c->r;
+    c->last_corr = -1;
     c->launches = 0;
     CU(cudaMemsetAsync(acc, 0, n * sizeof(double2), c->stream));
     float* stage = c->samp[c->samp_cur ^ 1];
@@ -1383,6 +1411,7 @@ int sslg_push_samples_async(sslg_ctx* c, const float* pcm, uint64_t nsamples, ui
     if (!pcm && nsamples) return set_err(SSLG_VALIDATION, "null argument");
     if (c->poisoned) return set_err(SSLG_VALIDATION, "stream stopped by a non-finite spectrum value; reset the window");
     TRY(check_device_gate(c));
+    TRY(ensure_slots(c));
     uint32_t frames = 0;
     TRY(sslg_samples_pending(c, nsamples, &frames, nullptr));
     const uint32_t subs = (frames + c->cfg.max_batch - 1) / c->cfg.max_batch;

@@ -181,6 +181,201 @@ int main() {
             }
         }
     }
+    // test_correlation.cpp:67-120 -- CorrelationWindow against brute force,
+    // the rebuild cadence, underfill and shape changes
+    {
+        auto random_frame = [](std::uint32_t index, std::size_t m, std::size_t bins, std::mt19937_64& rng) {
+            std::normal_distribution<double> nd;
+            ssl::SpectrumFrame f;
+            f.frame_index = index;
+            f.spectra.assign(m, std::vector<ssl::cfloat>(bins));
+            for (auto& ch : f.spectra)
+                for (auto& v : ch) v = ssl::cfloat(float(nd(rng)), float(nd(rng)));
+            return f;
+        };
+        const std::size_t m = 3, bins = 4, t = 5;
+        std::mt19937_64 rng(23);
+        ssl::CorrelationWindow window(t);
+        std::vector<ssl::SpectrumFrame> hist;
+        for (std::uint32_t i = 0; i < 17; ++i) {
+            hist.push_back(random_frame(i, m, bins, rng));
+            window.push(hist.back());
+            if (i + 1 < t) {
+                CHECK(!window.filled());
+                continue;
+            }
+            CHECK(window.filled());
+            const auto got = window.normalized();
+            CHECK(got.frame_index == i);
+            for (std::size_t b = 0; b < bins; ++b)
+                for (std::size_t r = 0; r < m; ++r)
+                    for (std::size_t c = 0; c < m; ++c) {
+                        ssl::cdouble want(0, 0);
+                        for (std::size_t k = hist.size() - t; k < hist.size(); ++k)
+                            want += ssl::cdouble(hist[k].spectra[r][b]) * std::conj(ssl::cdouble(hist[k].spectra[c][b]));
+                        want /= double(t);
+                        CHECK(std::abs(ssl::cdouble(got.bins[b](r, c)) - want) <= 1e-6 * (1.0 + std::abs(want)));
+                    }
+        }
+        ssl::CorrelationWindow frequent(4, 3), rare(4, 1000000);
+        std::mt19937_64 rng2(31);
+        for (std::uint32_t i = 0; i < 40; ++i) {
+            const auto f = random_frame(i, 2, 2, rng2);
+            frequent.push(f);
+            rare.push(f);
+            if (!frequent.filled()) continue;
+            const auto a = frequent.normalized(), b = rare.normalized();
+            for (std::size_t bin = 0; bin < 2; ++bin)
+                for (std::size_t q = 0; q < 4; ++q) CHECK(std::abs(a.bins[bin].data[q] - b.bins[bin].data[q]) <= 1e-6f);
+        }
+        ssl::CorrelationWindow small(3);
+        std::mt19937_64 rng3(5);
+        small.push(random_frame(0, 2, 2, rng3));
+        bool threw = false;
+        try {
+            small.normalized();
+        } catch (const ssl::ValidationError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        threw = false;
+        try {
+            small.push(random_frame(1, 3, 2, rng3));
+        } catch (const ssl::ValidationError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // test_gsvd.cpp:36-76 -- inverses, pivot-free elimination
+    {
+        ssl::NoiseModel piv;
+        piv.k.m = 2;
+        piv.k.bins.assign(1, ssl::CMatrix<float>(2, 2));
+        piv.k.bins[0](0, 1) = 1;
+        piv.k.bins[0](1, 0) = 1;
+        piv.prepare_inverses(ssl::Pivoting::partial);
+        const auto inv = piv.inverse_double(0);
+        CHECK(std::abs(inv(0, 1) - ssl::cdouble(1, 0)) <= 1e-14 && std::abs(inv(0, 0)) <= 1e-14);
+        bool threw = false;
+        try {
+            piv.prepare_inverses(ssl::Pivoting::none);
+        } catch (const ssl::NumericalError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        std::mt19937_64 rng(101);
+        std::normal_distribution<double> nd;
+        for (std::size_t n : {1, 2, 5, 8}) {
+            ssl::NoiseModel nm;
+            nm.k.m = std::uint32_t(n);
+            nm.k.bins.assign(1, ssl::CMatrix<float>(n, n));
+            ssl::CMatrix<double> a(n, n);
+            for (auto& z : a.data) z = {nd(rng), nd(rng)};
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) {
+                    ssl::cdouble v(0, 0);
+                    for (std::size_t q = 0; q < n; ++q) v += a(i, q) * std::conj(a(j, q));
+                    nm.k.bins[0](i, j) = ssl::cfloat(float(v.real() / n + (i == j ? 0.5 : 0)), float(v.imag() / n));
+                }
+            nm.prepare_inverses(ssl::Pivoting::partial);
+            const auto ki = nm.inverse_double(0);
+            double err = 0;
+            for (std::size_t i = 0; i < n; ++i)
+                for (std::size_t j = 0; j < n; ++j) {
+                    ssl::cdouble v(0, 0);
+                    for (std::size_t q = 0; q < n; ++q) v += ssl::cdouble(nm.k.bins[0](i, q)) * ki(q, j);
+                    err = std::max(err, std::abs(v - ssl::cdouble(i == j ? 1 : 0, 0)));
+                }
+            CHECK(err <= 1e-12);
+        }
+    }
+    // test_gsvd.cpp:159-223 -- E_r, the residual, budgets
+    {
+        std::mt19937_64 rng(127);
+        std::normal_distribution<double> nd;
+        ssl::CorrelationSet r;
+        r.m = 5;
+        r.bins.assign(1, ssl::CMatrix<float>(5, 5));
+        for (auto& z : r.bins[0].data) z = {float(nd(rng)), float(nd(rng))};
+        ssl::SolverConfig cfg;
+        cfg.compute_residual = true;
+        const auto noise = ssl::NoiseModel::identity(5, 1);
+        const auto got = ssl::gsvd_reference(noise, r, cfg);
+        const auto& g = got.bins[0];
+        CHECK(g.recon_residual >= 0.0 && g.recon_residual <= 1e-12);
+        double err = 0, ref = 0, def = 0;
+        for (std::size_t i = 0; i < 5; ++i)
+            for (std::size_t j = 0; j < 5; ++j) {
+                ssl::cdouble v(0, 0), u(0, 0);
+                for (std::size_t q = 0; q < 5; ++q) {
+                    v += g.e(i, q) * g.singular_values[q] * g.e_r(q, j);
+                    u += std::conj(g.e_r(q, i)) * g.e_r(q, j);  // E_r^H E_r
+                }
+                err += std::norm(v - ssl::cdouble(r.bins[0](i, j)));
+                ref += std::norm(ssl::cdouble(r.bins[0](i, j)));
+                def += std::norm(u - ssl::cdouble(i == j ? 1 : 0, 0));
+            }
+        CHECK(std::sqrt(err / ref) <= 1e-12 && std::sqrt(def) <= 1e-10);
+        ssl::SolverConfig tight;
+        tight.max_qr_sweeps = 1;
+        ssl::CorrelationSet r12;
+        r12.m = 12;
+        r12.bins.assign(1, ssl::CMatrix<float>(12, 12));
+        for (auto& z : r12.bins[0].data) z = {float(nd(rng)), float(nd(rng))};
+        CHECK(!ssl::gsvd(ssl::NoiseModel::identity(12, 1), r12, tight).bins[0].converged);
+        CHECK(ssl::gsvd(ssl::NoiseModel::identity(12, 1), r12).bins[0].converged);
+        // repeated solves reuse the noise model's device context
+        const auto again = ssl::gsvd_reference(noise, r, cfg);
+        CHECK(again.bins[0].singular_values == g.singular_values);
+        bool threw = false;
+        try {
+            ssl::SolverConfig bad;
+            bad.tolerance_scale = 0;
+            ssl::gsvd(noise, r, bad);
+        } catch (const ssl::ValidationError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // files: save/load round trips, NoiseModel::from_file, JSONL records
+    {
+        ssl::CorrelationSet k;
+        k.m = 2;
+        k.bins.assign(3, ssl::CMatrix<float>::identity(2));
+        k.bins[1](0, 1) = {0.25f, -0.5f};
+        k.bins[1](1, 0) = {0.25f, 0.5f};
+        ssl::save_correlation("/tmp/sslg_dropin_k.sslc", k, 7);
+        std::uint32_t t = 0;
+        const auto back = ssl::load_correlation("/tmp/sslg_dropin_k.sslc", &t);
+        CHECK(t == 7 && back.m == 2 && back.bins.size() == 3 && back.bins[1](0, 1) == k.bins[1](0, 1));
+        const auto nm = ssl::NoiseModel::from_file("/tmp/sslg_dropin_k.sslc");
+        CHECK(nm.k.bins[1](1, 0) == k.bins[1](1, 0));
+        ssl::SteeringField st;
+        st.m = 2;
+        st.bin_min = 3;
+        st.bin_max = 4;
+        st.directions = {{0, 0}, {90, 10.5}};
+        st.vectors = {{1, 0}, {0, 1}, {1, 1}, {0, -1}, {2, 0}, {0, 2}, {3, 3}, {-1, 0}};
+        ssl::save_steering(st, "/tmp/sslg_dropin_h.steer");
+        const auto s2 = ssl::load_steering("/tmp/sslg_dropin_h.steer");
+        CHECK(s2.m == 2 && s2.bin_min == 3 && s2.bin_max == 4 && s2.directions.size() == 2 &&
+              s2.directions[1].elevation_deg == 10.5 && s2.vectors == st.vectors);
+        bool threw = false;
+        try {
+            ssl::load_correlation("/tmp/sslg_dropin_missing.sslc");
+        } catch (const ssl::IoError&) {
+            threw = true;
+        }
+        CHECK(threw);
+        ssl::FrameEstimates fe;
+        fe.frame_index = 49;
+        fe.estimates.push_back({8, {40.0, 0.0}, 12.5, false});
+        fe.estimates.push_back({30, {150.0, 0.0}, 3.0, true});
+        CHECK(ssl::format_estimates_json(fe) ==
+              "{\"estimates\":[{\"azimuth_deg\":40.0,\"direction\":8,\"elevation_deg\":0.0,\"low_power\":false,"
+              "\"power\":12.5},{\"azimuth_deg\":150.0,\"direction\":30,\"elevation_deg\":0.0,\"low_power\":true,"
+              "\"power\":3.0}],\"frame\":49}");
+    }
     if (failures) {
         std::fprintf(stderr, "%d of %d checks failed\n", failures, checks);
         return 1;
