@@ -74,7 +74,59 @@ def parse():
                         "of per-bin powers (strong, BinShardedLocator)")
     p.add_argument("--arrays", type=int, default=1,
                    help="independent arrays (engines, one stream each) per GPU; >1 = BASELINE configs[4] (C5)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher/plumbing check without a GPU: gloo ranks, barrier + max-over-ranks timing of an "
+                        "empty step, the JSON line with n_gpus (tests/test_bench_contract.py)")
     return p.parse_args()
+
+
+def relaunch_if_needed(args) -> bool:
+    """`python bench.py --gpus N` (N > 1) outside torchrun starts the N
+    ranks itself: it re-executes under torch.distributed.run with one process
+    per GPU (127.0.0.1 rendezvous), forwards every argument and exits with the
+    launcher's status.  Under torchrun (WORLD_SIZE set) nothing happens."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
+
+
+def run_dry(args, rank, world):
+    """The multi-rank plumbing of the bench without a device: gloo process
+    group, barrier, an (empty) timed step per step, max over ranks, one JSON
+    line from rank 0 naming every rank that took part."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+    ms = (time.perf_counter() - t0) * 1e3
+    ranks = [rank]
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        got = [None] * world
+        dist.all_gather_object(got, rank)
+        ranks = got
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / max(1, args.steps), "dry_run": True,
+                          "ranks": ranks, "scaling": "weak"}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
@@ -229,9 +281,13 @@ def run_reference_arm(args, w, rank, world):
 
 def main():
     args = parse()
+    relaunch_if_needed(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
 
     from paper_2504_03373_b200 import synth
 
@@ -422,13 +478,13 @@ def main():
         achieved_tf = (alg["f_whiten"] + alg["f_jacobi"]) * blocks_per_launch / (jac_ms * 1e-3) / 1e12
         traffic = load_traffic()
         jac_traffic = None
-        parts = ["jacobi_prologue", "sweep_kernel", "jacobi_epilogue"]
-        if traffic and all(k in traffic for k in parts):  # ncu captures (--batch 8) scaled to this launch
+        # this config's own ncu capture (profiles/ncu_summary.json, keys "<config>:<kernel>"), per block, scaled
+        # to this launch; no capture of this config -> null (never another config's numbers)
+        parts = (["jacobi_prologue", "sweep_kernel", "jacobi_epilogue"] if w.m == 60 else ["jacobi_kernel"])
+        keys = [f"{args.config}:{k}" for k in parts]
+        if traffic and all(k in traffic for k in keys):
             jac_traffic = sum(traffic[k]["dram_bytes_per_launch"] / traffic[k].get("blocks_per_launch", 8)
-                              for k in parts) * blocks_per_launch
-        elif traffic and "jacobi_kernel" in traffic:
-            t = traffic["jacobi_kernel"]
-            jac_traffic = t["dram_bytes_per_launch"] / t.get("blocks_per_launch", 8) * blocks_per_launch
+                              for k in keys) * blocks_per_launch
         roofline = {
             "kernel": "GSVD solver: jacobi_kernel<60,1> (whitening A = K^-1 R + QRCP) -> sweep_kernel "
                       "(FP64 one-sided Jacobi sweeps) -> jacobi_kernel<60,3> (sigma, back-multiply, "
@@ -476,6 +532,11 @@ def main():
                        "l2": "flushed (256 MiB write) between timed steps" if not args.no_flush else "not flushed",
                        "parallelism": f"array-sharded x{world} (no data-path collective)"},
             "gsvd_us_per_block": 1e3 * (jac_ms + can_ms) / blocks_per_launch,
+            "gsvd_speedup_vs_reference": None if not cpu else {
+                "vs_1thread": cpu["gsvd_1thread_us"] / (1e3 * (jac_ms + can_ms) / blocks_per_launch),
+                "vs_allcore": cpu["gsvd_allcore_us"] / (1e3 * (jac_ms + can_ms) / blocks_per_launch),
+                "reference": "ssl::gsvd (batched float path) per block, noise inverses prepared outside the timer "
+                             "(bench.cpp:198-231), median of 5 calls x 5 blocks after a warm-up"},
             "gsvd_latency_us_single_block": gsvd_latency_us,
             "x_realtime": value / REALTIME_BLOCKS_PER_S,
             "target_hit_rate": hits,

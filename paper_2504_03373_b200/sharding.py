@@ -99,26 +99,45 @@ class BinShardedLocator:
         self.eng.set_noise_model(np.ascontiguousarray(k[self.lo:self.hi]))
         self.eng.set_steering(np.ascontiguousarray(h[:, self.lo:self.hi]), dirs, topo)
         self.max_batch = max_batch
+        self.pushed = 0
 
     def push(self, frames: np.ndarray):
+        """frames [F][m][B] complex64 (host).  The rank's bin slice goes to the
+        device in one copy; the pushes, the per-bin power copies, ONE
+        all-gather for every block of the call and the ordered integration
+        are all stream-ordered on the locator's stream -- the host waits only
+        when the estimates are read back."""
         import torch
 
-        results = []
-        for c0 in range(0, frames.shape[0], self.max_batch):
-            local = np.ascontiguousarray(frames[c0:c0 + self.max_batch, :, self.lo:self.hi])
-            with torch.cuda.stream(self.stream):
-                n = self.eng.push(local)["n"]  # local-bin estimates are superseded below
-                if n == 0:
-                    continue
-                p_local = torch.empty((n, self.hi - self.lo, self.dirs), dtype=torch.float64, device=self.device)
-                self.eng.copy_bin_power_device(p_local.data_ptr(), n)
-                self.stream.synchronize()
-                p_all = gather_bin_power(p_local, self.slices, self.group)
-                self.eng.integrate_peaks_device(p_all.data_ptr(), n, self.bins)
-                results.append(self.eng.read_results(n, power=True))
-        if not results:
+        frames = np.ascontiguousarray(frames, np.complex64)
+        nfr = frames.shape[0]
+        pushed0 = self.pushed
+        self.pushed += nfr
+        if nfr == 0:
             return dict(n=0)
-        out = {k: np.concatenate([r[k] for r in results]) for k in ("frame_index", "count", "idx", "power_est", "low",
-                                                                     "power")}
-        out["n"] = int(out["count"].shape[0])
+        local = np.ascontiguousarray(frames[:, :, self.lo:self.hi])
+        b_local = self.hi - self.lo
+        with torch.cuda.stream(self.stream):
+            x = torch.from_numpy(local.view(np.float32)).pin_memory().to(f"cuda:{self.device}", non_blocking=True)
+            chunks = []
+            for c0 in range(0, nfr, self.max_batch):
+                nf = min(self.max_batch, nfr - c0)
+                n = self.eng.push_device(x[c0:c0 + nf].data_ptr(), nf)  # no host synchronization
+                if n:
+                    p = torch.empty((n, b_local, self.dirs), dtype=torch.float64, device=self.device)
+                    self.eng.copy_bin_power_device(p.data_ptr(), n)
+                    chunks.append(p)
+            if not chunks:
+                return dict(n=0)
+            p_local = chunks[0] if len(chunks) == 1 else torch.cat(chunks)
+            p_all = gather_bin_power(p_local, self.slices, self.group)  # one collective per push
+            results = []
+            for c0 in range(0, p_all.shape[0], self.max_batch):
+                n = min(self.max_batch, p_all.shape[0] - c0)
+                self.eng.integrate_peaks_device(p_all[c0:c0 + n].data_ptr(), n, self.bins)
+                results.append(self.eng.read_results(n, power=True))
+        out = {k: np.concatenate([r[k] for r in results]) for k in ("count", "idx", "power_est", "low", "power")}
+        n = int(out["count"].shape[0])
+        out["n"] = n
+        out["frame_index"] = np.arange(pushed0 + nfr - n, pushed0 + nfr, dtype=np.uint32)
         return out

@@ -47,3 +47,11 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["metric"] == METRIC and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_gpus_flag_launches_the_ranks_itself():
+    """`python bench.py --gpus 2` outside torchrun starts two ranks itself
+    (torch.distributed.run, 127.0.0.1 rendezvous); --dry-run exercises that
+    launcher and the barrier / max-over-ranks plumbing with gloo, no GPU."""
+    d = run_bench("--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "0")
+    assert d["n_gpus"] == 2 and sorted(d["ranks"]) == [0, 1] and d["dry_run"] is True

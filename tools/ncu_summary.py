@@ -71,8 +71,12 @@ def main():
         if not (f.startswith("prof_") and f.endswith(".ncu-rep")):
             continue
         kern = f[len("prof_"):-len(".ncu-rep")]
+        # prof_<config>__<kernel>.ncu-rep -> key "<config>:<kernel>" (per-config traffic for bench.py)
+        key = kern.replace("__", ":", 1) if "__" in kern else kern
+        cfg = key.split(":")[0] if ":" in key else "c3"
+        bpl = 4 if cfg in ("c1", "c2") else 8
         d = raw(os.path.join(OUT, f))
-        lines = [f"# ncu --set full, kernel {kern} (one launch of the bench workload, --batch 8)"]
+        lines = [f"# ncu --set full, kernel {kern} (one launch of the bench workload, --batch {bpl})"]
         for k in KEYS:
             if k in d:
                 lines.append(f"{k:90s} {d[k][0]:>16s} {d[k][1]}")
@@ -82,8 +86,8 @@ def main():
         wr = to_si(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
         dur = to_si(*d["gpu__time_duration.sum"]) if "gpu__time_duration.sum" in d else None
         grid = to_si(*d["launch__grid_size"]) if "launch__grid_size" in d else None
-        summary[kern] = {"dram_bytes_per_launch": (rd or 0) + (wr or 0), "duration_s": dur, "grid": grid,
-                         "blocks_per_launch": 8, "source": f"profiles/{tag}/ncu_{kern}.txt"}
+        summary[key] = {"dram_bytes_per_launch": (rd or 0) + (wr or 0), "duration_s": dur, "grid": grid,
+                        "blocks_per_launch": bpl, "source": f"profiles/{tag}/ncu_{kern}.txt"}
     lc = os.path.join(OUT, "launches.csv")
     if os.path.exists(lc):
         tot = defaultdict(float)
