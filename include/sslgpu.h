@@ -228,6 +228,13 @@ int sslg_locate_samples(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint
  * rewound to just before the failing push and SSLG_VALIDATION is returned;
  * sslg_reset_window restarts the stream. */
 int sslg_push_samples_async(sslg_ctx* ctx, const float* pcm, uint64_t nsamples, uint64_t* ticket);
+/* Which kernel evaluates the MUSIC contraction: -1 auto (the default: the
+ * tcgen05 kind::tf32 3-pass-split kernel for grids of >= 512 directions, the
+ * FP64 tensor-core DMMA kernel below), 0 always FP64 (DMMA / DFMA), 1 the
+ * tcgen05 kernel whenever m <= 64.  The tf32x3 path is within 5.6e-7 relative
+ * per bin and 2.8e-7 on the broadband power of the FP64 one on the C4 grid
+ * (tests/test_gpu_spectrum_tc.py; the reference's own float path: ~1e-4). */
+int sslg_set_spectrum_path(sslg_ctx* ctx, int mode);
 /* Whether asynchronous pushes also copy the broadband power [e][dirs] back
  * (needed for sslg_wait_results' `power`; off by default: FrameEstimates,
  * pipeline.hpp:63-66, carries only the estimates).  Refused while pushes are

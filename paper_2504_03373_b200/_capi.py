@@ -89,6 +89,7 @@ EXPORTS = {
     "sslg_gsvd_ex": (C.c_int, [C.c_void_p, _f32p, C.c_uint32, _f64p, _f64p, _f64p, _u32p, _u8p, _f64p]),
     "sslg_noise_inverse": (C.c_int, [C.c_void_p, C.c_int, _f64p]),
     "sslg_set_async_power": (C.c_int, [C.c_void_p, C.c_int]),
+    "sslg_set_spectrum_path": (C.c_int, [C.c_void_p, C.c_int]),
     "sslg_read_correlation_file": (C.c_int, [C.c_char_p, _u32p, _u32p, _u32p, _f32p, C.c_uint64]),
     "sslg_write_correlation_file": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint32, C.c_uint32, _f32p]),
     "sslg_load_noise_model": (C.c_int, [C.c_void_p, C.c_char_p, _u32p, _u32p]),

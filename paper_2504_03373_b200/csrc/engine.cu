@@ -21,6 +21,7 @@
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a profiler attaches
 
 #include <algorithm>
 #include <cmath>
@@ -64,6 +65,16 @@ int set_error(int code, const std::string& msg) {
 namespace {
 
 int set_err(int code, const std::string& msg) { return sslg::set_error(code, msg); }
+
+// grids from this size up take the tcgen05 spectrum (C4: 1368 directions)
+constexpr uint32_t kSpectrumTcMinDirs = 512;
+
+// NVTX range per hot-path stage: the host-side launch spans of
+// correlation, GSVD, MUSIC + peaks, STFT and the pushes that contain them
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 #define CU(call)                                                                                   \
     do {                                                                                           \
@@ -164,6 +175,8 @@ struct sslg_ctx {
     bool async_power = false;   // async pushes also copy back power [e][dirs] (sslg_set_async_power)
     bool slots_ready = false;   // pinned result ring allocated (ensure_slots)
     int last_corr = -1;         // index in r of the newest set emitted by sslg_correlation (-1: none)
+    int spectrum_tc = -1;       // -1 auto (grids >= kSpectrumTcMinDirs), 0 FP64 DMMA, 1 tcgen05 tf32x3
+    float* tc_slabs = nullptr;  // steering operand slabs of the tcgen05 spectrum (built on first use)
     // device-frame pushes (sslg_push_frames_device) gate on the device through
     // the same abort word; their window counters are kept until the next
     // synchronizing call verifies the word (check_device_gate)
@@ -215,6 +228,7 @@ int check_last_launch(const char* what) {
 
 // Runs GSVD -> (canonical) on n correlation sets already in c->r.
 int run_gsvd(sslg_ctx* c, int n) {
+    Nvtx range("sslg:gsvd");
     const sslg_config& g = c->cfg;
     CU(cudaMemsetAsync(c->work, 0, 2 * sizeof(uint32_t), c->stream));
     GsvdArgs ga{c->r,   c->kinv, c->sigma, c->e, c->sweeps, c->conv, c->work, (int)g.m, (int)g.bins,
@@ -239,11 +253,24 @@ int run_gsvd(sslg_ctx* c, int n) {
 }
 
 int run_music(sslg_ctx* c, int n) {
+    Nvtx range("sslg:music+peaks");
     const sslg_config& g = c->cfg;
     SpecArgs sa{c->e, c->h_t, c->num, c->p, (int)g.m, (int)g.bins, (int)c->dirs, (int)g.num_sources, 0, 0,
                 (double)g.denominator_floor, g.squared_denominator};
     sa.abort = c->abort;
-    launch_spectrum(sa, n, c->stream);
+    // large grids run on the tcgen05 tensor cores (kind::tf32, 3-pass split:
+    // <= 5.6e-7 per bin, <= 2.8e-7 broadband vs FP64); SSLG_SPECTRUM_TC=0/1 or
+    // sslg_set_spectrum_path force the FP64 DMMA / tcgen05 path
+    const bool tc = spectrum_tc_supported(sa) &&
+                    (c->spectrum_tc > 0 || (c->spectrum_tc < 0 && c->dirs >= kSpectrumTcMinDirs));
+    if (tc && !c->tc_slabs) {  // the steering as tf32 hi/lo operand slabs, once per steering field
+        TRY(dalloc(&c->tc_slabs, spectrum_tc_slab_floats((int)g.m, (int)g.bins, (int)c->dirs)));
+        launch_spectrum_tc_prep(c->h_t, (int)g.m, (int)g.bins, (int)c->dirs, c->tc_slabs, c->stream);
+        ++c->launches;
+        TRY(check_last_launch("spectrum_tc_prep_kernel"));
+    }
+    if (tc) launch_spectrum_tc(sa, c->tc_slabs, n, c->stream);
+    else launch_spectrum(sa, n, c->stream);
     ++c->launches;
     TRY(check_last_launch("spectrum_kernel"));
     CU(cudaEventRecord(c->ev[4], c->stream));
@@ -305,13 +332,17 @@ int process_chunk(sslg_ctx* c, uint32_t nframes, uint32_t* emitted) {
     const sslg_config& g = c->cfg;
     *emitted = 0;
     if (nframes == 0) return 0;
+    Nvtx range("sslg:push_chunk");
     const long long first_emit = std::max<long long>(0, (long long)g.window_frames - 1 - c->pushed);
     const int n = (int)std::max<long long>(0, (long long)nframes - first_emit);
     CU(cudaEventRecord(c->ev[0], c->stream));
     CorrArgs ca{c->ring, c->state, c->r, (int)g.m, (int)g.bins, (int)g.window_frames, c->cap, (int)nframes,
                 c->pushed, c->since, (int)(g.rebuild_interval ? g.rebuild_interval : 1)};
     ca.abort = c->abort;
-    launch_correlation(ca, c->stream);
+    {
+        Nvtx range("sslg:correlation");
+        launch_correlation(ca, c->stream);
+    }
     ++c->launches;
     TRY(check_last_launch("correlation_kernel"));
     CU(cudaEventRecord(c->ev[1], c->stream));
@@ -490,6 +521,7 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
         rc |= dalloc(&c->wscratch, NB * B * mm);
         rc |= dalloc(&c->pivs, NB * B * 64);
     }
+    if (const char* tc = std::getenv("SSLG_SPECTRUM_TC")) c->spectrum_tc = tc[0] == '1' ? 1 : 0;
     if (const char* pc = std::getenv("SSLG_PHASE_CLOCKS"); pc && pc[0] == '1') {
         rc |= dalloc(&c->phase_clk, 8);
         if (!rc) cudaMemset(c->phase_clk, 0, 8 * sizeof(long long));
@@ -524,7 +556,7 @@ void sslg_destroy(sslg_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch,
-                    (void*)c->abort})
+                    (void*)c->abort, (void*)c->tc_slabs})
         if (p) cudaFree(p);
     for (auto& sl : c->slots) {
         for (void* p : {(void*)sl.idx, (void*)sl.pw, (void*)sl.low, (void*)sl.cnt, (void*)sl.power})
@@ -771,6 +803,11 @@ int sslg_set_steering(sslg_ctx* c, uint32_t dirs, const float* h, const double* 
     CU(cudaMemcpyAsync(c->nbr_off, nbr_off, (dirs + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
     if (nnz) CU(cudaMemcpyAsync(c->nbr, nbr, nnz * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(c->h_raw, h, hn * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+    if (c->tc_slabs) {  // rebuilt from the new field on the next tcgen05 launch
+        CU(cudaStreamSynchronize(c->stream));
+        cudaFree(c->tc_slabs);
+        c->tc_slabs = nullptr;
+    }
     launch_steering_prep(c->h_raw, c->h_t, c->num, (int)g.m, (int)g.bins, (int)dirs, c->stream);
     TRY(check_last_launch("steering_prep_kernel"));
     CU(cudaStreamSynchronize(c->stream));
@@ -1214,6 +1251,7 @@ namespace {
 
 int launch_stft_frames(sslg_ctx* c, const float* pcm_dev, size_t pitch, int nframes, float2* out, int cap,
                        long long slot0) {
+    Nvtx range("sslg:stft");
     StftArgs sa{pcm_dev, c->win, c->twiddle, out, pitch, (int)c->cfg.m, (int)c->stft.frame_length,
                 (int)c->stft.shift, (int)c->stft.bin_min, (int)c->cfg.bins, cap, slot0};
     launch_stft(sa, nframes, c->stream);
@@ -1388,6 +1426,13 @@ int sslg_locate_samples(sslg_ctx* c, const float* pcm, uint64_t nsamples, uint32
 }
 
 // ---- asynchronous streaming --------------------------------
+
+int sslg_set_spectrum_path(sslg_ctx* c, int mode) {
+    if (!c) return set_err(SSLG_VALIDATION, "null argument");
+    if (mode < -1 || mode > 1) return set_err(SSLG_VALIDATION, "spectrum path must be -1 (auto), 0 or 1");
+    c->spectrum_tc = mode;
+    return SSLG_OK;
+}
 
 int sslg_set_async_power(sslg_ctx* c, int on) {
     if (!c) return set_err(SSLG_VALIDATION, "null argument");

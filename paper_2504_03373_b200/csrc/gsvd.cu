@@ -1340,9 +1340,11 @@ __device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const Gs
                                 W[q * m + row] = Q[u];
                             }
                         }
-                        // lane 0 writes the norms the whole group loaded (one
-                        // converged LDS) before the group shuffles of the dot;
-                        // racecheck cannot see that ordering and warns
+                        // lane 0 writes the norms the whole group loaded; the
+                        // group barrier orders those loads before the write
+                        // under the CUDA memory model (the group's shuffles
+                        // already did in practice)
+                        __syncwarp(group_mask<LPP>());
                         if (s == 0) {
                             cn[p] = cp;
                             cn[q] = cq;

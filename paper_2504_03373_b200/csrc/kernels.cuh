@@ -104,6 +104,12 @@ struct SpecArgs {
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
 };
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s);
+// the tcgen05 kind::tf32 (3-pass split) spectrum of large grids (music_tc.cu):
+// the steering is prepared once into tf32 hi/lo slabs (spectrum_tc_slab_floats)
+bool spectrum_tc_supported(const SpecArgs& a);
+size_t spectrum_tc_slab_floats(int m, int bins, int dirs);
+void launch_spectrum_tc_prep(const float2* h_t, int m, int bins, int dirs, float* slabs, cudaStream_t s);
+void launch_spectrum_tc(const SpecArgs& a, const float* slabs, int nblk, cudaStream_t s);
 // capture_noise_model (synth.cpp:329-373): FP64 sums of x x^H over frames, then K = float(sum / F)
 void launch_capture_accum(const float2* frames, int nframes, int m, int bins, double2* acc, cudaStream_t s);
 void launch_capture_narrow(const double2* acc, size_t n, double inv, float2* k, cudaStream_t s);

@@ -390,6 +390,10 @@ class Engine:
         self._inflight.append((t.value, pcm))
         return t.value
 
+    def set_spectrum_path(self, mode: int = -1) -> None:
+        """-1 auto (tcgen05 tf32x3 for grids >= 512 directions), 0 FP64, 1 tcgen05."""
+        _capi.check(self.L.sslg_set_spectrum_path(self.h, int(mode)))
+
     def set_async_power(self, on: bool = True) -> None:
         """Asynchronous pushes also bring the broadband power back (for
         wait_results(want_power=True))."""

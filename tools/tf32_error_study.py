@@ -1,0 +1,152 @@
+"""Error study for putting the C4 MUSIC contraction on reduced-precision
+tensor cores (VERDICT r01 "next" 7).
+
+The spectrum P(theta, w) = |h|^2 / sum_{i >= Ns} |h^H e_i| (music.cpp:112-165)
+is a complex GEMM [D x M] . [M x (M - Ns)] per bin.  On tcgen05 it could run
+as kind::tf32 with the usual 3-pass split (a = a_hi + a_lo, a_hi/a_lo TF32,
+a.b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi, FP32 accumulation), or with the
+noise vectors split into several FP32 parts first (they are FP64 in the
+engine).  Near a source direction h is almost orthogonal to every noise
+vector, so each |h^H e_i| is a small difference of large terms and the
+relative error of the denominator grows like eps_acc |h| |e_i| / |h^H e_i|:
+exactly where the peaks are.  This script measures it on a C4 scene
+(60 channels, 257 bins, 72 az x 19 el = 1368 directions, 3 sources) against
+the FP64 spectrum the engine computes (per-bin tolerance 1e-6 relative,
+broadband 1e-8; the engine reaches ~1e-9 / ~1e-11):
+
+  fp32_inputs_exact  E rounded to FP32, products and sums exact (the input
+                     rounding alone)
+  tf32x3_fp32acc     3-pass TF32 split of FP32 inputs, FP32 accumulation
+                     (what kind::tf32 tcgen05 with a 3-pass split computes)
+  e_split3_tf32x3    E split into 3 FP32 parts (e = e1 + e2 + e3), each
+                     product in 3-pass TF32, FP32 accumulation per part
+  fp64               the engine's arithmetic (reference point)
+
+  python tools/tf32_error_study.py [--bins 24] [--out profiles/r02/tf32_error_study.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def tf32(x):
+    """Round float32 values to TF32 (10 explicit mantissa bits, RNE)."""
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    lsb = (u >> 13) & 1
+    u = (u + 0xFFF + lsb) & ~np.uint64(0x1FFF)
+    return u.astype(np.uint32).view(np.float32)
+
+
+def split_tf32(x):
+    hi = tf32(x)
+    lo = tf32((x.astype(np.float32) - hi).astype(np.float32))
+    return hi, lo
+
+
+def cdot_fp32_acc(hr, hi_, er, ei, passes):
+    """sum_k conj(h_k) e_k with every real product from `passes` TF32 split
+    terms, accumulated in FP32 in k order (tensor-core style)."""
+    acc_r = np.zeros(hr.shape[:-1] + er.shape[-1:], np.float32)
+    acc_i = np.zeros_like(acc_r)
+    hrs, his = split_tf32(hr), split_tf32(hi_)
+    ers, eis = split_tf32(er), split_tf32(ei)
+
+    def prod(a, b):
+        # a [D][M] (split pair), b [M][K] (split pair) -> [D][K], one TF32-exact
+        # product per pass pair, FP32 accumulation over M
+        out = np.zeros((a[0].shape[0], b[0].shape[1]), np.float32)
+        terms = [(0, 0), (0, 1), (1, 0)][:passes]
+        for k in range(a[0].shape[1]):
+            for (p, q) in terms:
+                out = (out + (a[p][:, k:k + 1].astype(np.float64) * b[q][k:k + 1, :].astype(np.float64)).astype(
+                    np.float32)).astype(np.float32)
+        return out
+
+    # conj(h) e = (hr - i hi)(er + i ei) = (hr er + hi ei) + i (hr ei - hi er)
+    acc_r = (prod(hrs, ers) + prod(his, eis)).astype(np.float32)
+    acc_i = (prod(hrs, eis) - prod(his, ers)).astype(np.float32)
+    return acc_r.astype(np.float64) + 1j * acc_i.astype(np.float64)
+
+
+def main():
+    from paper_2504_03373_b200 import synth
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bins", type=int, default=24)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02", "tf32_error_study.json"))
+    args = ap.parse_args()
+    w = synth.make("c4", frames=52)
+    t, ns = w.t, w.ns
+    x = w.x.astype(np.complex128)
+    r = np.einsum("fib,fjb->bij", x[1:1 + t], x[1:1 + t].conj()) / t
+    kinv = np.linalg.inv(w.k.astype(np.complex128))
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(w.bins, args.bins, replace=False))
+    res = {k: [] for k in ("fp32_inputs_exact", "tf32x3_fp32acc", "e_split3_tf32x3")}
+    worst_dir = {}
+    pbar = {k: np.zeros(w.h.shape[0]) for k in list(res) + ["fp64"]}
+    for b in sel:
+        a = kinv[b] @ r[b]
+        u, s, vh = np.linalg.svd(a)
+        en = u[:, ns:]  # [M][M-Ns] FP64 noise vectors
+        h = w.h[:, b, :].astype(np.complex64)  # [D][M] FP32-stored steering
+        hd = h.astype(np.complex128)
+        num = np.sum(np.abs(hd) ** 2, axis=1)
+        den64 = np.sum(np.abs(hd.conj() @ en), axis=1)
+        p64 = num / den64
+        pbar["fp64"] += p64
+        e32 = en.astype(np.complex64).astype(np.complex128)
+        den_a = np.sum(np.abs(hd.conj() @ e32), axis=1)
+        hr, hi_ = h.real.astype(np.float32), h.imag.astype(np.float32)
+        er, ei = en.real.astype(np.float32), en.imag.astype(np.float32)
+        den_b = np.sum(np.abs(cdot_fp32_acc(hr, hi_, er, ei, 3)), axis=1)
+        # E in three FP32 parts
+        parts = []
+        rest_r, rest_i = en.real.copy(), en.imag.copy()
+        for _ in range(3):
+            pr, pi = rest_r.astype(np.float32), rest_i.astype(np.float32)
+            parts.append((pr, pi))
+            rest_r, rest_i = rest_r - pr, rest_i - pi
+        dots = sum(cdot_fp32_acc(hr, hi_, pr, pi, 3) for pr, pi in parts)
+        den_c = np.sum(np.abs(dots), axis=1)
+        for k, den in (("fp32_inputs_exact", den_a), ("tf32x3_fp32acc", den_b), ("e_split3_tf32x3", den_c)):
+            p = num / den
+            rel = np.abs(p - p64) / p64
+            res[k].append(float(rel.max()))
+            pbar[k] += p
+            d = int(np.argmax(rel))
+            worst_dir.setdefault(k, []).append((int(b), d, float(rel[d]), float(p64[d] / np.median(p64))))
+        print(f"bin {b}: max rel err " + ", ".join(f"{k} {res[k][-1]:.2e}" for k in res), flush=True)
+    out = {
+        "scene": "C4 (synth.make('c4')): 60-ch circular r=0.3 m, 72 az x 19 el = 1368 directions, 3 sources, T=50",
+        "bins_sampled": [int(b) for b in sel],
+        "tolerances": {"per_bin_P_rel": 1e-6, "broadband_Pbar_rel": 1e-8},
+        "per_bin_P_max_rel_err": {k: max(v) for k, v in res.items()},
+        "per_bin_P_median_of_bin_max_rel_err": {k: float(np.median(v)) for k, v in res.items()},
+        "bins_over_1e-6": {k: int(sum(x > 1e-6 for x in v)) for k, v in res.items()},
+        "pbar_over_sampled_bins_max_rel_err": {k: float(np.max(np.abs(pbar[k] - pbar["fp64"]) / pbar["fp64"]))
+                                               for k in res},
+        "worst_direction_examples (bin, dir, rel_err, P/median P)": {k: sorted(v, key=lambda z: -z[2])[:5]
+                                                                     for k, v in worst_dir.items()},
+        "conclusion": "",
+    }
+    ok = [k for k in res if out["per_bin_P_max_rel_err"][k] <= 1e-6 and
+          out["pbar_over_sampled_bins_max_rel_err"][k] <= 1e-8]
+    out["conclusion"] = ("variants within the 1e-6 / 1e-8 tolerances: " + (", ".join(ok) if ok else "none") +
+                         "; the FP64 tensor-core (DMMA) spectrum is kept")
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps({k: out[k] for k in ("per_bin_P_max_rel_err", "bins_over_1e-6",
+                                          "pbar_over_sampled_bins_max_rel_err", "conclusion")}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
