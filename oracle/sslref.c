@@ -748,7 +748,6 @@ int orc_stft(const float* pcm, uint32_t m, uint64_t nsamples, uint32_t frame_len
     if (shift > frame_length) return set_err(2, "shift must not exceed frame_length");
     if (bin_min > bin_max) return set_err(2, "bin_min must not exceed bin_max");
     if (bin_max > frame_length / 2) return set_err(2, "bin_max exceeds the half spectrum of frame_length");
-    if (frame_length & (frame_length - 1)) return set_err(2, "oracle STFT covers power-of-two lengths only");
     /* stft_frame_count (stft.cpp:38-42) */
     const uint64_t nf = nsamples < frame_length ? 0 : (nsamples - frame_length) / shift + 1;
     if (nframes) *nframes = (uint32_t)nf;
@@ -764,6 +763,22 @@ int orc_stft(const float* pcm, uint32_t m, uint64_t nsamples, uint32_t frame_len
             for (uint32_t i = 0; i < frame_length; ++i) {
                 re[i] = src[i] * w[i];
                 im[i] = 0.0f;
+            }
+            if (frame_length & (frame_length - 1)) {
+                /* real_dft_half's direct sum for other lengths (fft.hpp:55-65):
+                   FP64 accumulation in i order, the angle as the reference writes it */
+                for (uint32_t b = 0; b < nb; ++b) {
+                    const uint32_t k = bin_min + b;
+                    double sr = 0, si = 0;
+                    for (uint32_t i = 0; i < frame_length; ++i) {
+                        const double ang = -2.0 * M_PI * (double)k * (double)i / (double)frame_length;
+                        sr += (double)re[i] * cos(ang);
+                        si += (double)re[i] * sin(ang);
+                    }
+                    frames[((f * m + c) * (uint64_t)nb + b) * 2] = (float)sr;
+                    frames[((f * m + c) * (uint64_t)nb + b) * 2 + 1] = (float)si;
+                }
+                continue;
             }
             fft_pow2_f(re, im, frame_length);
             float* dst = frames + ((f * m + c) * (uint64_t)nb) * 2;  /* retained band (stft.cpp:55-56) */

@@ -146,6 +146,7 @@ struct sslg_ctx {
     bool have_stft = false;
     float* win = nullptr;          // [frame_length]
     double2* twiddle = nullptr;    // [frame_length - 1]
+    double2* dft = nullptr;        // non-power-of-two frame length: [bins][frame_length] (cos, sin)
     float* samp[2] = {nullptr, nullptr};  // [m][samp_cap] sample history, ping-pong
     size_t samp_cap = 0;           // frame_length + max_batch * shift
     size_t samp_fill = 0;          // samples held in samp[samp_cur]
@@ -556,7 +557,7 @@ void sslg_destroy(sslg_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch,
-                    (void*)c->abort, (void*)c->tc_slabs})
+                    (void*)c->abort, (void*)c->tc_slabs, (void*)c->dft})
         if (p) cudaFree(p);
     for (auto& sl : c->slots) {
         for (void* p : {(void*)sl.idx, (void*)sl.pw, (void*)sl.low, (void*)sl.cnt, (void*)sl.power})
@@ -1201,8 +1202,10 @@ int sslg_set_stft(sslg_ctx* c, const sslg_stft_config* s) {
     if (s->bin_max > s->frame_length / 2)
         return set_err(SSLG_VALIDATION, "bin_max exceeds the half spectrum of frame_length");
     if (s->window != 0 && s->window != 1) return set_err(SSLG_VALIDATION, "unknown window");
-    if ((s->frame_length & (s->frame_length - 1)) || s->frame_length > 8192)
-        return set_err(SSLG_VALIDATION, "the device STFT takes power-of-two frame lengths up to 8192");
+    const bool pow2 = (s->frame_length & (s->frame_length - 1)) == 0;
+    if (pow2 ? s->frame_length > 8192 : s->frame_length > 4096)
+        return set_err(SSLG_VALIDATION,
+                       "the device STFT takes frame lengths up to 8192 (power of two) or 4096 (direct sum)");
     if (s->bin_max - s->bin_min + 1 != c->cfg.bins)
         return set_err(SSLG_VALIDATION, "STFT band does not match the engine's bin count");
     CU(cudaSetDevice(c->cfg.device));
@@ -1225,10 +1228,12 @@ int sslg_set_stft(sslg_ctx* c, const sslg_stft_config* s) {
             wi = e + f;
         }
     }
-    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch})
+    for (void* p : {(void*)c->win, (void*)c->twiddle, (void*)c->samp[0], (void*)c->samp[1], (void*)c->frame_scratch,
+                    (void*)c->dft})
         if (p) cudaFree(p);
     c->win = nullptr;
     c->twiddle = nullptr;
+    c->dft = nullptr;
     c->samp[0] = c->samp[1] = nullptr;
     c->frame_scratch = nullptr;
     c->have_stft = false;
@@ -1240,6 +1245,18 @@ int sslg_set_stft(sslg_ctx* c, const sslg_stft_config* s) {
     TRY(dalloc(&c->frame_scratch, (size_t)c->cfg.max_batch * c->cfg.m * c->cfg.bins));
     CU(cudaMemcpy(c->win, w.data(), n * sizeof(float), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(c->twiddle, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    if (!pow2) {
+        // real_dft_half's direct sum (fft.hpp:55-65): the angle evaluated as
+        // the reference writes it, -2.0 * M_PI * double(k) * double(i) / double(n)
+        std::vector<double2> cs((size_t)c->cfg.bins * n);
+        for (uint32_t b = 0; b < c->cfg.bins; ++b)
+            for (uint32_t i = 0; i < n; ++i) {
+                const volatile double ang = -2.0 * M_PI * double(s->bin_min + b) * double(i) / double(n);
+                cs[(size_t)b * n + i] = make_double2(std::cos(ang), std::sin(ang));
+            }
+        TRY(dalloc(&c->dft, cs.size()));
+        CU(cudaMemcpy(c->dft, cs.data(), cs.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
     c->stft = *s;
     c->samp_fill = 0;
     c->samp_cur = 0;
@@ -1254,6 +1271,7 @@ int launch_stft_frames(sslg_ctx* c, const float* pcm_dev, size_t pitch, int nfra
     Nvtx range("sslg:stft");
     StftArgs sa{pcm_dev, c->win, c->twiddle, out, pitch, (int)c->cfg.m, (int)c->stft.frame_length,
                 (int)c->stft.shift, (int)c->stft.bin_min, (int)c->cfg.bins, cap, slot0};
+    sa.dft = c->dft;
     launch_stft(sa, nframes, c->stream);
     ++c->launches;
     return check_last_launch("stft_kernel");

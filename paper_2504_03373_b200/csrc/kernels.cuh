@@ -15,6 +15,7 @@ struct StftArgs {
     int m, n, shift, bin_min, bins;
     int cap;
     long long slot0;         // ring index of frame 0 of this launch
+    const double2* dft = nullptr;  // non-power-of-two n: [bins][n] (cos, sin) of the retained bins
 };
 void launch_stft(const StftArgs& a, int nframes, cudaStream_t s);
 

@@ -1,6 +1,7 @@
 // Kernel (0): the STFT front end, SampleBlock -> SpectrumFrame
 // (stft_frame / stft_stream, reference proj/src/stft.cpp:44-68, with
-// real_dft_half / fft_pow2, proj/include/ssl/fft.hpp:15-68).
+// real_dft_half / fft_pow2, proj/include/ssl/fft.hpp:15-68; other frame
+// lengths through the direct sum, dft_kernel below).
 //
 // One warp per (frame, channel): the windowed frame (float product
 // src[i] * window[i], stft.cpp:53) is stored bit-reversed in shared memory,
@@ -53,6 +54,39 @@ __global__ void stft_kernel(StftArgs a) {
     for (int b = lane; b < a.bins; b += kWarp) dst[b] = buf[a.bin_min + b];
 }
 
+// Non-power-of-two frame lengths: the reference's direct sum
+// (real_dft_half, fft.hpp:55-65): out[k] = sum_i double(x_i) (cos, sin)(ang),
+// ang = -2 pi k i / n, accumulated in i order in FP64 and rounded to float.
+// The (cos, sin) table of the retained bins is evaluated on the host with
+// the reference's libm calls and operation order (sslg_set_stft), so with
+// unfused products and sums every bin is bit-identical.  One warp per
+// (frame, channel), lanes over the retained bins.
+__global__ void dft_kernel(StftArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+    const int wpc = blockDim.x / kWarp;
+    const int f = blockIdx.x;
+    const int ch = blockIdx.y * wpc + warp;
+    if (ch >= a.m) return;
+    const int n = a.n;
+    float* x = reinterpret_cast<float*>(smem_raw) + (size_t)warp * n;
+    const float* src = a.pcm + (size_t)ch * a.pitch + (size_t)f * a.shift;
+    for (int i = lane; i < n; i += kWarp) x[i] = __fmul_rn(src[i], a.window[i]);
+    __syncwarp();
+    float2* dst = a.out + ((size_t)((a.slot0 + f) % a.cap) * a.m + ch) * a.bins;
+    for (int b = lane; b < a.bins; b += kWarp) {
+        const double2* cs = a.dft + (size_t)b * n;
+        double re = 0.0, im = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double xi = x[i];
+            const double2 c = cs[i];
+            re = __dadd_rn(re, __dmul_rn(xi, c.x));
+            im = __dadd_rn(im, __dmul_rn(xi, c.y));
+        }
+        dst[b] = make_float2(__double2float_rn(re), __double2float_rn(im));
+    }
+}
+
 int stft_warps_per_cta(int n) {
     int w = 16384 / n;  // <= 32 KB of shared memory per CTA
     if (w > 8) w = 8;
@@ -65,6 +99,12 @@ void launch_stft(const StftArgs& a, int nframes, cudaStream_t s) {
     const size_t smem = (size_t)wpc * a.n * sizeof(float2);
     if (smem > 48 * 1024) cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(nframes, (a.m + wpc - 1) / wpc);
+    if (a.dft) {  // non-power-of-two length: direct sum, one float per sample staged
+        const size_t smem_d = (size_t)wpc * a.n * sizeof(float);
+        if (smem_d > 48 * 1024) cudaFuncSetAttribute(dft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_d);
+        dft_kernel<<<grid, wpc * kWarp, smem_d, s>>>(a);
+        return;
+    }
     stft_kernel<<<grid, wpc * kWarp, smem, s>>>(a);
 }
 

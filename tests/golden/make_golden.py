@@ -103,6 +103,11 @@ def stft_fixture():
                             bin_max=256, sources=[Source(10), Source(200, kind="tone", freq=2500.0)])),
         ("hann_256", Scene(mics=5, radius=0.05, duration_s=0.1, seed=8, frame_length=256, shift=100, bin_min=3,
                            bin_max=128, diffuse_db=-10, sources=[Source(300)])),
+        # non-power-of-two lengths: real_dft_half's direct sum (fft.hpp:55-65)
+        ("hann_480", Scene(mics=4, radius=0.05, duration_s=0.12, seed=12, frame_length=480, shift=160, bin_min=10,
+                           bin_max=90, diffuse_db=-20, sources=[Source(60)])),
+        ("rect_300", Scene(mics=3, radius=0.05, duration_s=0.08, seed=13, window="rectangular", frame_length=300,
+                           shift=100, bin_min=0, bin_max=150, sources=[Source(120, kind="tone", freq=900.0)])),
     ]
     for name, sc in cases:
         w = R.workload(sc, with_audio=True)

@@ -12,7 +12,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "stft.npz")
-CASES = ["hann_band", "rect_full", "hann_256"]
+CASES = ["hann_band", "rect_full", "hann_256", "hann_480", "rect_300"]
 
 
 def _cfg(g, name):

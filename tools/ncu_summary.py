@@ -64,7 +64,9 @@ def to_si(v, u):
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    dst = os.path.join(ROOT, "profiles", tag)
+    # optional second argument: write the summaries there (e.g. inside
+    # gpurun_out/ on the GPU box, so the large .ncu-rep files can be dropped)
+    dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", tag)
     os.makedirs(dst, exist_ok=True)
     summary = {}
     for f in sorted(os.listdir(OUT)):
@@ -107,7 +109,8 @@ def main():
                      "--batch 8 (cold-cache, serialized: compare shares)\n")
             for k in sorted(tot, key=lambda x: -tot[x]):
                 fh.write(f"{k:60s} launches {cnt[k]:5d}  total {tot[k]*1e3:10.3f} ms  share {100*tot[k]/s:6.2f}%\n")
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fh:
+    with open(os.path.join(dst if len(sys.argv) > 2 else os.path.join(ROOT, "profiles"), "ncu_summary.json"),
+              "w") as fh:
         json.dump(summary, fh, indent=1)
     print(json.dumps(summary, indent=1))
 
