@@ -113,8 +113,9 @@ def test_stft_validation():
     eng = ssl.Engine(2, 73)
     with pytest.raises(ValidationError):
         eng.set_stft(ssl.StftConfig(512, 160, "hann", 16, 90))  # band != engine bins
+    eng.set_stft(ssl.StftConfig(480, 160, "hann", 16, 88))  # other lengths: the direct sum (fft.hpp:55-65)
     with pytest.raises(ValidationError):
-        eng.set_stft(ssl.StftConfig(480, 160, "hann", 16, 88))  # not a power of two on the device
+        eng.set_stft(ssl.StftConfig(5000, 160, "hann", 16, 88))  # direct sum capped at 4096 on the device
     with pytest.raises(ValidationError):
         eng.set_stft(ssl.StftConfig(512, 600, "hann", 16, 88))  # shift > frame_length
     eng.set_stft(ssl.StftConfig())
