@@ -96,9 +96,11 @@ __device__ __forceinline__ void rr_pair(int r, int g, int n, int& p, int& q) {
     if (g == 0) {
         a = n - 1;
         b = r;
-    } else {
-        a = (r + g) % (n - 1);
-        b = (r - g + (n - 1)) % (n - 1);
+    } else {  // r < n - 1 and g < n / 2: one conditional subtraction replaces the modulo
+        a = r + g;
+        if (a >= n - 1) a -= n - 1;
+        b = r - g + (n - 1);
+        if (b >= n - 1) b -= n - 1;
     }
     p = a < b ? a : b;
     q = a < b ? b : a;

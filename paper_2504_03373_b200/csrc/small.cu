@@ -1,5 +1,5 @@
-// GSVD of small arrays (m <= 16: BASELINE configs C1 = 8 and C2 = 16
-// channels) with one WARP per (block, bin) instead of one CTA.
+// GSVD of small arrays (m <= 8: BASELINE config C1) with one WARP per
+// (block, bin) instead of one CTA.
 //
 // At m = 8 an SVD is ~30 kFLOP; the CTA-wide solver (gsvd.cu) spent most of
 // its time in block barriers and serial phases.  Here a warp owns a bin:
@@ -29,7 +29,8 @@ constexpr int kSmallWarps = 4;  // warps (bins) per CTA
 
 template <int MC>
 struct SmallScratch {
-    double2 w[MC * MC];  // column-major: w[j * MC + i] = A(i, j)
+    double2 w[MC * MC];  // column-major: w[j * MC + i] = A(i, j) (R widened, before the whitening)
+    double2 k[MC * MC];  // K^-1 row-major (stride MC)
     double cn[MC];
     double sig[MC];
     int perm[MC];  // rank -> column
@@ -52,13 +53,31 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 8) small_jacobi_kernel(GsvdA
     const float2* r = a.r + (size_t)blk * mm;
     const double2* kinv = a.kinv + (size_t)bin * mm;
 
-    // 1. A = K^-1 R; padding rows / columns (m < MC) are zero
+    // 1. A = K^-1 R; padding rows / columns (m < MC) are zero.  R and K^-1
+    //    are staged in shared memory by coalesced loads first
     for (int e = lane; e < MC * MC; e += 32) {
+        const int i = e / MC, j = e % MC;
+        const bool in = i < m && j < m;
+        S.w[j * MC + i] = in ? f2d(r[i * m + j]) : make_double2(0, 0);  // R(i, j), column-major
+        S.k[i * MC + j] = in ? kinv[i * m + j] : make_double2(0, 0);
+    }
+    __syncwarp();
+    constexpr int EPL = MC * MC / 32;  // entries per lane
+    double2 av[EPL];
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+        const int e = lane + 32 * u;
         const int i = e % MC, j = e / MC;
         double2 acc = make_double2(0, 0);
-        if (i < m && j < m)
-            for (int k = 0; k < m; ++k) acc = cadd(acc, cmul(kinv[i * m + k], f2d(r[k * m + j])));
-        S.w[j * MC + i] = acc;
+#pragma unroll 4
+        for (int k = 0; k < MC; ++k) acc = cadd(acc, cmul(S.k[i * MC + k], S.w[j * MC + k]));
+        av[u] = acc;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < EPL; ++u) {
+        const int e = lane + 32 * u;
+        S.w[(e / MC) * MC + (e % MC)] = av[u];
     }
     __syncwarp();
 
@@ -185,13 +204,17 @@ __global__ void __launch_bounds__(32 * kSmallWarps, 8) small_jacobi_kernel(GsvdA
     }
 }
 
-bool small_jacobi_supported(const GsvdArgs& a) { return a.m <= 16; }
+// m <= 8 only: at m = 16 (C2) the warp solver measured slower than the CTA
+// solver (48 vs 30 us per block): without the QR preconditioning it needs
+// 10.2 instead of 6.0 sweeps, and C2's bins often carry tied / vanishing
+// groups that then take the separate canonical_kernel pass (0.49 ms per 32
+// blocks) instead of the CTA solver's fused pickers
+bool small_jacobi_supported(const GsvdArgs& a) { return a.m <= 8; }
 
 void launch_small_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
     const int n = nblk * a.bins;
     const int grid = (n + kSmallWarps - 1) / kSmallWarps;
-    if (a.m <= 8) small_jacobi_kernel<8><<<grid, 32 * kSmallWarps, 0, s>>>(a, n);
-    else small_jacobi_kernel<16><<<grid, 32 * kSmallWarps, 0, s>>>(a, n);
+    small_jacobi_kernel<8><<<grid, 32 * kSmallWarps, 0, s>>>(a, n);
 }
 
 }  // namespace sslg
