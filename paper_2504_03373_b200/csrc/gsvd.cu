@@ -1642,6 +1642,196 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
     }
 }
 
+// The sweeps of the split solver in a recursive bipartite ordering (m = 60
+// padded to 64 columns, 32 processors of four lanes, 15 rows per lane):
+//   level S = 32, 16, 8, 4, 2, 1 (groups of S processors, 2S columns):
+//     every processor keeps a resident BOTTOM column in registers for the
+//     whole level, and the group's S TOP columns sit in S slots; each round
+//     pairs every bottom with a different top, so that over the level's S
+//     rounds every top meets every bottom of the group once: for S >= 8 in
+//     blocks of eight warp-local rounds (warp wi of the group visits the
+//     tops of warp wi + k/8's slots, processor pw slot (pw + k) mod 8), so a
+//     CTA barrier is needed only between blocks, not between rounds;
+//     then the group splits: its tops form one group of S/2 processors (the
+//     lower half takes the tops of the upper slots as its new bottoms) and
+//     its bottoms the other (the lower half's old bottoms become the upper
+//     group's tops, in those slots).
+// 32 + 16 + 8 + 4 + 2 + 1 = 63 rounds visit each of the 64*63/2 pairs once.
+// Slots hold column ids; W stays in shared memory by column id, so a round
+// loads and stores ONE column per processor (the top) where the circle
+// ordering (run_sweeps) loads and stores both, and 8 CTA barriers per sweep
+// replace 59.  Every sweep starts from the same arrangement: carrying the
+// end-of-sweep arrangement into the next sweep changes the cyclic order and
+// costs a sweep (numpy on the C3 matrices: 8.27 against 7.18 counted sweeps;
+// this ordering 7.12 in numpy, 7.18 on the GPU; the circle ordering 7.09 /
+// 7.06).  Measured against sweep_kernel on C3: 206k vs 214k SM cycles per
+// CTA-sweep (three CTAs per SM), 20.70 vs 21.04 ms of solver per 32 blocks:
+// halving the shared-memory traffic and removing 51 barriers per sweep
+// gains only 4% per sweep -- the round is bound by its own dependent chain
+// (dot product, shuffle reduction, rotation parameters) at three warps per
+// scheduler with the FP64 pipe 52% busy.
+// The rotation, skip and convergence rules are the reference's
+// (gsvd.cpp:642-674); the Gram certificate is run_sweeps'.
+constexpr int kBipRows = 15;  // 60 rows over 4 lanes
+
+// the warps of this thread's S-processor group (eight processors per warp)
+__device__ __forceinline__ void bip_group_sync(int S, int warp) {
+    if (S >= 32) {
+        __syncthreads();
+    } else {  // S = 16: a warp pair
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp >> 1)) : "memory");
+    }
+}
+
+template <int MC>
+__global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
+    static_assert(MC == 4 * kBipRows, "bipartite-ordered sweeps: m = 60");
+    if (a.abort && *a.abort) return;
+    constexpr int m = MC, R = kBipRows;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* W = reinterpret_cast<double2*>(smem_raw);  // [column id][row]
+    __shared__ double cn[64];
+    __shared__ int slot_id[32];
+    __shared__ int s_rots;
+    __shared__ unsigned s_maxrel;
+    const int tid = threadIdx.x;
+    const int g = tid >> 2, s = tid & 3;  // processor, lane in it
+    const long long clk0 = clock64();
+    double2* wg = a.wscratch + (size_t)blockIdx.x * m * m;
+    for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
+    if (tid == 0) {
+        s_rots = 0;
+        s_maxrel = 0u;
+    }
+    __syncthreads();
+    const int total_pairs = m * (m - 1) / 2;
+    int prev_rots = 1 << 30;
+    bool prev_maxrel = true;
+    int sweep = 0;
+    bool converged = false;
+    while (sweep < a.max_sweeps) {
+        // fresh squared column norms (gsvd.cpp:633-637): four lanes per column
+        {
+            const int j = tid >> 1, part = tid & 1;
+            double v = 0.0;
+            if (j < m)
+                for (int i = part; i < m; i += 2) v = fma(W[j * m + i].x, W[j * m + i].x, fma(W[j * m + i].y, W[j * m + i].y, v));
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            if (part == 0) cn[j] = j < m ? v : 0.0;
+        }
+        if (s == 0) slot_id[g] = 2 * g;  // the sweep's starting arrangement: tops 2g
+        __syncthreads();
+        // the Gram certificate of a probably rotation-free sweep (see run_sweeps)
+        if (sweep > 0 && (2 * prev_rots < total_pairs || !prev_maxrel) &&
+            gram_converged<MC, 4>(W, m, cn, 0.0, a.tol2)) {
+            converged = true;
+            break;
+        }
+        int qid = 2 * g + 1;  // resident bottom
+        double2 Q[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) Q[u] = qid < m ? W[qid * m + s + 4 * u] : make_double2(0, 0);
+        double cq = cn[qid];
+        bool qdirty = false;
+        __syncthreads();  // every thread has read s_rots / s_maxrel
+        if (tid == 0) {
+            s_rots = 0;
+            s_maxrel = 0u;
+        }
+        int myrots = 0;
+        double mymax = 0.0;
+        bool rot = false;
+#pragma unroll 1
+        for (int S = 32; S >= 1; S >>= 1) {
+            const int b = g & ~(S - 1), pos = g - b;
+            const int wi = pos >> 3, pw = pos & 7, nw = S >> 3;  // S >= 8: warp in the group, processor in the warp
+#pragma unroll 1
+            for (int k = 0; k < S; ++k) {
+                // S >= 8: blocks of eight warp-local rounds over one slot
+                // region (the tops of warp wi + k/8 of the group)
+                const int sl = S >= 8 ? b + (((wi + (k >> 3)) & (nw - 1)) << 3) + ((pw + k) & 7)
+                                      : b + ((pos + k) & (S - 1));
+                const int pid = slot_id[sl];
+                if (pid < m && qid < m) {
+                    double2 P[R];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) P[u] = W[pid * m + s + 4 * u];
+                    double cp = cn[pid];
+                    if (rotate_pair<R, 4>(P, Q, cp, cq, 0.0, s, m, mymax, a.tol2)) {
+#pragma unroll
+                        for (int u = 0; u < R; ++u) W[pid * m + s + 4 * u] = P[u];
+                        __syncwarp(group_mask<4>());  // the group's loads of cn[pid] precede the write
+                        if (s == 0) {
+                            cn[pid] = cp;
+                            ++myrots;
+                        }
+                        qdirty = true;
+                        rot = true;
+                    }
+                }
+                if (S >= 16 && (k & 7) == 7) {
+                    bip_group_sync(S, tid >> 5);  // the next block reads another warp's slots
+                } else {
+                    __syncwarp();
+                }
+            }
+            if (S == 1) break;
+            // split: the lower half swaps its bottom with the top in slot
+            // b + S/2 + pos (that top becomes its bottom, its bottom a top of
+            // the upper half's group)
+            const int h = S >> 1;
+            if (pos < h) {
+                const int sl = b + h + pos;
+                const int nid = slot_id[sl];
+                if (qid < m) {
+                    if (qdirty) {
+#pragma unroll
+                        for (int u = 0; u < R; ++u) W[qid * m + s + 4 * u] = Q[u];
+                    }
+                    __syncwarp(group_mask<4>());
+                    if (s == 0) cn[qid] = cq;
+                }
+                qdirty = false;
+#pragma unroll
+                for (int u = 0; u < R; ++u) Q[u] = nid < m ? W[nid * m + s + 4 * u] : make_double2(0, 0);
+                cq = cn[nid];
+                __syncwarp(group_mask<4>());
+                if (s == 0) slot_id[sl] = qid;
+                qid = nid;
+            }
+            if (S >= 16) {
+                bip_group_sync(S, tid >> 5);
+            } else {
+                __syncwarp();
+            }
+        }
+        // the resident bottoms go home
+        if (qid < m && qdirty) {
+#pragma unroll
+            for (int u = 0; u < R; ++u) W[qid * m + s + 4 * u] = Q[u];
+        }
+        ++sweep;
+        if (s == 0 && myrots) {
+            atomicAdd(&s_rots, myrots);
+            if (mymax > 0) atomicMax(&s_maxrel, 1u);
+        }
+        if (!__syncthreads_or(rot)) {
+            converged = true;
+            break;
+        }
+        prev_rots = s_rots;
+        prev_maxrel = s_maxrel != 0u;
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[e];
+    if (tid == 0) {
+        a.sweeps[blockIdx.x] = (uint32_t)sweep;
+        a.conv[blockIdx.x] = converged ? 1 : 0;
+        if (a.phase_clk)
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk + 2), (unsigned long long)(clock64() - clk0));
+    }
+}
+
 int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
     auto launch = [&](auto kern, int threads, int mc) {
         const size_t smem = (size_t)a.m * a.m * sizeof(double2) + (size_t)scratch_entries(mc) * sizeof(double2);
@@ -1652,8 +1842,13 @@ int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
         // split around the 128-thread sweep kernel
         launch(jacobi_kernel<60, 1>, jac_threads<60>(), 60);
         const size_t smem = (size_t)60 * 60 * sizeof(double2);
-        cudaFuncSetAttribute(sweep_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        sweep_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
+        if (a.legacy_sweep) {
+            cudaFuncSetAttribute(sweep_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            sweep_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(sweep_bip_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            sweep_bip_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
+        }
         launch(jacobi_kernel<60, 3>, jac_threads<60>(), 60);
         return 3;
     }
