@@ -335,8 +335,31 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
         }
         __syncthreads();
         if (cs.collapsed) return;  // uniform: written before the barrier above
-        // row solve q_rb = (d_rb - sum_{a<b} q_ra conj(L_ba)) / L_bb, four lanes per row
-        {
+        // row solve q_rb = (d_rb - sum_{a<b} q_ra conj(L_ba)) / L_bb
+        if constexpr (MMA) {  // one thread per row, two partial sums
+            for (int r = t; r < m; r += nt) {
+                for (int b = 0; b < nd; ++b) {
+                    double2 acc0 = make_double2(0, 0), acc1 = make_double2(0, 0);
+                    const double2* lb = G + b * (b + 1) / 2;
+                    int a = 0;
+                    for (; a + 2 <= b; a += 2) {
+                        const double2 q0 = W[cs.dropped[a] * m + r], l0 = lb[a];
+                        const double2 q1 = W[cs.dropped[a + 1] * m + r], l1 = lb[a + 1];
+                        acc0.x = fma(q0.x, l0.x, fma(q0.y, l0.y, acc0.x));
+                        acc0.y = fma(q0.y, l0.x, fma(-q0.x, l0.y, acc0.y));
+                        acc1.x = fma(q1.x, l1.x, fma(q1.y, l1.y, acc1.x));
+                        acc1.y = fma(q1.y, l1.x, fma(-q1.x, l1.y, acc1.y));
+                    }
+                    if (a < b) {
+                        const double2 q0 = W[cs.dropped[a] * m + r], l0 = lb[a];
+                        acc0.x = fma(q0.x, l0.x, fma(q0.y, l0.y, acc0.x));
+                        acc0.y = fma(q0.y, l0.x, fma(-q0.x, l0.y, acc0.y));
+                    }
+                    double2* w = W + cs.dropped[b] * m + r;
+                    *w = cscale(invd[b], csub(*w, cadd(acc0, acc1)));
+                }
+            }
+        } else {  // four lanes per row
             const int part = t & 3;
             const unsigned gm = 0xfu << ((t & 31) & ~3);
             for (int r = t >> 2; r < m; r += nt / 4) {
@@ -365,73 +388,98 @@ __device__ void complete_basis(double2* W, double2* G, int m_rt, CanonScratchFor
     }
 }
 
-// Fast path of the picker: when the first d candidates (rows 0..d-1 of
-// conj(N)) are all accepted in the first pass — the usual case, a unit
-// vector projects onto a d-dimensional span with norm ~sqrt(d/m) >> 0.05 —
-// the reference's sequential two-pass Gram-Schmidt over them is the QR
-// factorization Y = Z R of the d x d candidate matrix, and candidate j's
-// residual norm is R_jj.  One warp forms G = Y^H Y, runs the Cholesky
-// G = R^H R checking R_jj > 0.05 n0_j at every step (the acceptance test of
-// pick_orthonormal, gsvd.cpp:404-436), and forms Z = Y R^-1.  Returns false
-// (nothing written) when a candidate would be rejected; the caller then runs
-// the sequential picker.  No block barrier inside: warp 0 only.
+// Fast path of the picker.  The reference's sequential two-pass Gram-Schmidt
+// over the candidates in index order (pick_orthonormal, gsvd.cpp:404-436,
+// first threshold pass) is a Cholesky factorization of the candidates' Gram
+// matrix G = Y^H Y in which a candidate is accepted when its residual norm
+// R_jj exceeds 0.05 n0_j and a rejected candidate is simply skipped (its row
+// never enters the trailing updates).  One warp forms G for the first
+// K = min(m, d + 8) candidates (rows of conj(N)), factors it with skipping
+// until d are accepted, and forms the accepted vectors' coordinates
+// Z = Y_sel R^-1.  Returns false (nothing written) when fewer than d of the K
+// candidates pass; the caller then runs the sequential picker over all m.
+// No block barrier inside: warp 0 only.
 template <class CS>
 __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_norm0, CS& cs) {
     __shared__ int s_ok;
+    __shared__ int s_sel[kZMax];
     const int t = threadIdx.x;
     if (t < kWarp) {
         const int lane = t;
-        // G[a][b] = y_a^H y_b,  y_j[k] = conj(W[cols[k]][j])
-        for (int e = lane; e < d * d; e += kWarp) {
-            const int a = e / d, b = e % d;
+        const int K = min(m, d + 8);
+        // G[a][b] = y_a^H y_b (a <= b < K),  y_j[k] = conj(W[cols[k]][j])
+        for (int e = lane; e < K * K; e += kWarp) {
+            const int a = e / K, b = e % K;
             if (b < a) continue;
             double gx = 0, gy = 0;
             for (int k = 0; k < d; ++k) {
                 const double2 wa = W[cs.cols[k] * m + a], wb = W[cs.cols[k] * m + b];
-                // conj(y_a) y_b = wa * conj(wb)
                 gx = fma(wa.x, wb.x, fma(wa.y, wb.y, gx));
                 gy = fma(wa.y, wb.x, fma(-wa.x, wb.y, gy));
             }
-            G[a * d + b] = make_double2(gx, gy);
+            G[a * K + b] = make_double2(gx, gy);
         }
         __syncwarp();
-        if (lane < d) cs.norm0[lane] = unit_norm0 ? 1.0 : sqrt(G[lane * d + lane].x);
-        __syncwarp();
-        bool ok = true;
-        for (int j = 0; j < d && ok; ++j) {
-            const double gjj = G[j * d + j].x;
-            const double n0 = cs.norm0[j];
+        // candidate norms before projection: lanes own j = lane, lane + 32
+        const double n0a = unit_norm0 ? 1.0 : (lane < K ? sqrt(G[lane * K + lane].x) : 0.0);
+        const double n0b = unit_norm0 ? 1.0 : (lane + kWarp < K ? sqrt(G[(lane + kWarp) * K + lane + kWarp].x) : 0.0);
+        int taken = 0;
+        for (int j = 0; j < K && taken < d; ++j) {
+            const double n0j = __shfl_sync(0xffffffffu, j < kWarp ? n0a : n0b, j & 31);
+            const double gjj = G[j * K + j].x;
             const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
-            if (!(n0 > 1e-140) || !(rjj > 0.05 * n0) || !(rjj > 0)) {
-                ok = false;
-                break;
-            }
+            if (!(n0j > 1e-140) || !(rjj > 0.05 * n0j) || !(rjj > 0)) continue;  // rejected: skipped (warp-uniform)
             const double inv = 1.0 / rjj;
-            for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
+            for (int b = j + 1 + lane; b < K; b += kWarp) G[j * K + b] = cscale(inv, G[j * K + b]);
             __syncwarp();
-            // trailing upper triangle: G[a][b] -= conj(R[j][a]) R[j][b], j < a <= b
-            const int n = d - j - 1;
-            for (int e = lane; e < n * n; e += kWarp) {
-                const int a = j + 1 + e / n, b = j + 1 + e % n;
-                if (b < a) continue;
-                const double2 ra = G[j * d + a], rb = G[j * d + b];
-                double2& g = G[a * d + b];
-                g.x -= fma(ra.x, rb.x, ra.y * rb.y);
-                g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+            // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b];
+            // four rows per batch, loads first (row j is read-only here)
+            for (int b = j + 1 + lane; b < K; b += kWarp) {
+                const double2 rb = G[j * K + b];
+                int a = j + 1;
+                for (; a + 4 <= b + 1; a += 4) {
+                    double2 ra[4], g[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        ra[u] = G[j * K + a + u];
+                        g[u] = G[(a + u) * K + b];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        g[u].x -= fma(ra[u].x, rb.x, ra[u].y * rb.y);
+                        g[u].y -= fma(ra[u].x, rb.y, -ra[u].y * rb.x);
+                        G[(a + u) * K + b] = g[u];
+                    }
+                }
+                for (; a <= b; ++a) {
+                    const double2 ra = G[j * K + a];
+                    double2& g = G[a * K + b];
+                    g.x -= fma(ra.x, rb.x, ra.y * rb.y);
+                    g.y -= fma(ra.x, rb.y, -ra.y * rb.x);
+                }
             }
             if (lane == 0) {
-                G[j * d + j] = make_double2(rjj, 0.0);
-                cs.nrm[j] = inv;
+                G[j * K + j] = make_double2(rjj, 0.0);
+                cs.nrm[taken] = inv;
+                s_sel[taken] = j;
             }
+            ++taken;
             __syncwarp();
         }
-        if (ok && lane < d) {  // Z = Y R^-1 column by column, lane = coordinate
+        const bool ok = taken == d;
+        if (ok && lane < d) {  // Z = Y_sel R_sel^-1 column by column, lane = coordinate
             const int k = lane;
             for (int tt = 0; tt < d; ++tt) {
-                const double2 w = W[cs.cols[k] * m + tt];
-                double2 acc = make_double2(w.x, -w.y);  // y_tt[k]
-                for (int s2 = 0; s2 < tt; ++s2) acc = csub(acc, cmul(cs.z[k][s2], G[s2 * d + tt]));
-                cs.z[k][tt] = cscale(cs.nrm[tt], acc);
+                const int jt = s_sel[tt];
+                const double2 w = W[cs.cols[k] * m + jt];
+                double2 acc0 = make_double2(w.x, -w.y), acc1 = make_double2(0, 0);  // y_jt[k]
+                int s2 = 0;
+                for (; s2 + 2 <= tt; s2 += 2) {
+                    acc0 = csub(acc0, cmul(cs.z[k][s2], G[s_sel[s2] * K + jt]));
+                    acc1 = csub(acc1, cmul(cs.z[k][s2 + 1], G[s_sel[s2 + 1] * K + jt]));
+                }
+                if (s2 < tt) acc0 = csub(acc0, cmul(cs.z[k][s2], G[s_sel[s2] * K + jt]));
+                cs.z[k][tt] = cscale(cs.nrm[tt], cadd(acc0, acc1));
             }
         }
         if (lane == 0) s_ok = ok ? 1 : 0;
@@ -489,10 +537,26 @@ __device__ __forceinline__ bool chol_group(double2* G, double* n0b, double* ivb,
         const double inv = 1.0 / rjj;
         for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
         __syncwarp();
-        // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b]
+        // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b];
+        // four rows per batch, loads first (row j is read-only here)
         for (int b = j + 1 + lane; b < d; b += kWarp) {
             const double2 rb = G[j * d + b];
-            for (int a = j + 1; a <= b; ++a) {
+            int a = j + 1;
+            for (; a + 4 <= b + 1; a += 4) {
+                double2 ra[4], g[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    ra[u] = G[j * d + a + u];
+                    g[u] = G[(a + u) * d + b];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    g[u].x -= fma(ra[u].x, rb.x, ra[u].y * rb.y);
+                    g[u].y -= fma(ra[u].x, rb.y, -ra[u].y * rb.x);
+                    G[(a + u) * d + b] = g[u];
+                }
+            }
+            for (; a <= b; ++a) {
                 const double2 ra = G[j * d + a];
                 double2& g = G[a * d + b];
                 g.x -= fma(ra.x, rb.x, ra.y * rb.y);
