@@ -427,9 +427,9 @@ __device__ bool pick_fast(const double2* W, double2* G, int m, int d, bool unit_
         for (int j = 0; j < K && taken < d; ++j) {
             const double n0j = __shfl_sync(0xffffffffu, j < kWarp ? n0a : n0b, j & 31);
             const double gjj = G[j * K + j].x;
-            const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
+            const double inv = gjj > 1e-300 ? fast_rsqrt(gjj) : 0.0;
+            const double rjj = gjj * inv;
             if (!(n0j > 1e-140) || !(rjj > 0.05 * n0j) || !(rjj > 0)) continue;  // rejected: skipped (warp-uniform)
-            const double inv = 1.0 / rjj;
             for (int b = j + 1 + lane; b < K; b += kWarp) G[j * K + b] = cscale(inv, G[j * K + b]);
             __syncwarp();
             // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b];
@@ -532,9 +532,10 @@ __device__ __forceinline__ bool chol_group(double2* G, double* n0b, double* ivb,
     for (int j = 0; j < d; ++j) {
         const double gjj = G[j * d + j].x;
         const double n0 = n0b[j];
-        const double rjj = gjj > 0 ? sqrt(gjj) : 0.0;
+        // 1 / R_jj and R_jj from one refined rsqrt (the step's serial chain)
+        const double inv = gjj > 1e-300 ? fast_rsqrt(gjj) : 0.0;
+        const double rjj = gjj * inv;
         if (!(n0 > 1e-140) || !(rjj > 0.05 * n0) || !(rjj > 0)) return false;  // warp-uniform
-        const double inv = 1.0 / rjj;
         for (int b = j + 1 + lane; b < d; b += kWarp) G[j * d + b] = cscale(inv, G[j * d + b]);
         __syncwarp();
         // trailing upper triangle, column b per lane: G[a][b] -= conj(R[j][a]) R[j][b];
