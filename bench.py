@@ -480,15 +480,18 @@ def main():
         jac_traffic = None
         # this config's own ncu capture (profiles/ncu_summary.json, keys "<config>:<kernel>"), per block, scaled
         # to this launch; no capture of this config -> null (never another config's numbers)
-        parts = (["jacobi_prologue", "sweep_kernel", "jacobi_epilogue"] if w.m == 60 else ["jacobi_kernel"])
+        parts = (["jacobi_prologue", "sweep_bip_kernel", "jacobi_epilogue"] if w.m == 60
+                 else ["small_jacobi_kernel"] if w.m <= 16 else ["jacobi_kernel"])
         keys = [f"{args.config}:{k}" for k in parts]
         if traffic and all(k in traffic for k in keys):
             jac_traffic = sum(traffic[k]["dram_bytes_per_launch"] / traffic[k].get("blocks_per_launch", 8)
                               for k in keys) * blocks_per_launch
         roofline = {
-            "kernel": "GSVD solver: jacobi_kernel<60,1> (whitening A = K^-1 R + QRCP) -> sweep_kernel "
-                      "(FP64 one-sided Jacobi sweeps) -> jacobi_kernel<60,3> (sigma, back-multiply, "
-                      "canonical bases); achieved over the three launches",
+            "kernel": ("GSVD solver: jacobi_kernel<60,1> (whitening A = K^-1 R + QRCP) -> sweep_bip_kernel "
+                       "(FP64 one-sided Jacobi sweeps) -> jacobi_kernel<60,3> (sigma, back-multiply, "
+                       "canonical bases); achieved over the three launches" if w.m == 60 else
+                       "GSVD solver: small_jacobi_kernel (one lane group per bin: whitening, one-sided Jacobi, "
+                       "sort, canonical bases)" if w.m <= 16 else "GSVD solver: jacobi_kernel"),
             "bound": "fp64", "achieved": achieved_tf, "peak": fp64, "unit": "TFLOP/s",
             "frac": achieved_tf / fp64 if fp64 else None, "traffic": jac_traffic,
             "peak_kind": "measured in-run (DFMA microbenchmark, sslg_probe_fp64_tflops); "

@@ -178,7 +178,6 @@ struct sslg_ctx {
     int last_corr = -1;         // index in r of the newest set emitted by sslg_correlation (-1: none)
     int spectrum_tc = -1;       // -1 auto (grids >= kSpectrumTcMinDirs), 0 FP64 DMMA, 1 tcgen05 tf32x3
     float* tc_slabs = nullptr;  // steering operand slabs of the tcgen05 spectrum (built on first use)
-    int legacy_sweep = 0;       // SSLG_LEGACY_SWEEP=1: shared-memory sweep kernel at m = 60 (A/B measurement)
     int small_cta = 0;          // SSLG_SMALL_CTA=1: m <= 16 on the CTA solver (A/B measurement)
     // device-frame pushes (sslg_push_frames_device) gate on the device through
     // the same abort word; their window counters are kept until the next
@@ -242,7 +241,6 @@ int run_gsvd(sslg_ctx* c, int n) {
     ga.pivs = c->pivs;
     ga.tol2 = 1e-28 * (double)g.tolerance_scale * (double)g.tolerance_scale;
     ga.force_cta = c->small_cta;
-    ga.legacy_sweep = c->legacy_sweep;
     c->launches += launch_jacobi(ga, n, c->stream);
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
@@ -528,7 +526,6 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     }
     if (const char* tc = std::getenv("SSLG_SPECTRUM_TC")) c->spectrum_tc = tc[0] == '1' ? 1 : 0;
     if (const char* sm = std::getenv("SSLG_SMALL_CTA")) c->small_cta = sm[0] == '1';
-    if (const char* ls = std::getenv("SSLG_LEGACY_SWEEP")) c->legacy_sweep = ls[0] == '1';
     if (const char* pc = std::getenv("SSLG_PHASE_CLOCKS"); pc && pc[0] == '1') {
         rc |= dalloc(&c->phase_clk, 8);
         if (!rc) cudaMemset(c->phase_clk, 0, 8 * sizeof(long long));

@@ -1678,35 +1678,6 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     }
 }
 
-// The sweeps of the split solver: 4-lane pair groups with 16 rows per lane,
-// 128 threads and only W in shared memory, so three bins share an SM
-// (tools/ubench/sweep.cu -DSB_L4: 1471 SM-cycles per bin-round against 1638
-// for the fused 8-lane layout at two bins per SM).
-template <int MC>
-__global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
-    if (a.abort && *a.abort) return;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int m = MC;
-    double2* W = reinterpret_cast<double2*>(smem_raw);
-    __shared__ double cn[kMaxM];
-    const int blk = blockIdx.x, tid = threadIdx.x;
-    const long long clk0 = clock64();
-    double2* wg = a.wscratch + (size_t)blk * m * m;
-    for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
-    __syncthreads();
-    int sweep = 0;
-    bool converged = false;
-    double drop = 0.0;
-    run_sweeps<MC, 4>(W, m, cn, a.precondition && a.ascratch, a, sweep, converged, drop);
-    for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[e];
-    if (tid == 0) {
-        a.sweeps[blk] = (uint32_t)sweep;
-        a.conv[blk] = converged ? 1 : 0;
-        if (a.phase_clk)  // sweeps phase (SSLG_PHASE_CLOCKS)
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.phase_clk + 2), (unsigned long long)(clock64() - clk0));
-    }
-}
-
 // The sweeps of the split solver in a recursive bipartite ordering (m = 60
 // padded to 64 columns, 32 processors of four lanes, 15 rows per lane):
 //   level S = 32, 16, 8, 4, 2, 1 (groups of S processors, 2S columns):
@@ -1729,7 +1700,8 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_kernel(GsvdArgs a) {
 // end-of-sweep arrangement into the next sweep changes the cyclic order and
 // costs a sweep (numpy on the C3 matrices: 8.27 against 7.18 counted sweeps;
 // this ordering 7.12 in numpy, 7.18 on the GPU; the circle ordering 7.09 /
-// 7.06).  Measured against sweep_kernel on C3: 206k vs 214k SM cycles per
+// 7.06).  Measured against the circle-ordered kernel it replaced (128
+// threads, run_sweeps<60, 4> on W in shared memory) on C3: 206k vs 214k SM cycles per
 // CTA-sweep (three CTAs per SM), 20.70 vs 21.04 ms of solver per 32 blocks:
 // halving the shared-memory traffic and removing 51 barriers per sweep
 // gains only 4% per sweep -- the round is bound by its own dependent chain
@@ -1907,13 +1879,8 @@ int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
         // split around the 128-thread sweep kernel
         launch(jacobi_kernel<60, 1>, jac_threads<60>(), 60);
         const size_t smem = (size_t)60 * 60 * sizeof(double2);
-        if (a.legacy_sweep) {
-            cudaFuncSetAttribute(sweep_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            sweep_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
-        } else {
-            cudaFuncSetAttribute(sweep_bip_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            sweep_bip_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
-        }
+        cudaFuncSetAttribute(sweep_bip_kernel<60>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sweep_bip_kernel<60><<<nblk * a.bins, 128, smem, s>>>(a);
         launch(jacobi_kernel<60, 3>, jac_threads<60>(), 60);
         return 3;
     }

@@ -63,7 +63,6 @@ struct GsvdArgs {
     const unsigned int* abort = nullptr;  // nonzero: a failed gate earlier on the stream, skip (async path)
     double2* wscratch = nullptr;  // [nblk][bins][m][m] W between the split solver kernels (m = 60)
     int* pivs = nullptr;          // [nblk][bins][64] QR column pivots between them
-    int legacy_sweep = 0;         // m = 60: the shared-memory sweep kernel (A/B, SSLG_LEGACY_SWEEP=1)
     int force_cta = 0;            // m <= 8: use the CTA solver instead of the warp solver (A/B, SSLG_SMALL_CTA=1)
     double tol2 = 1e-28;          // no-rotation test |a_pq|^2 <= tol2 |w_p|^2 |w_q|^2 (gsvd.cpp:648);
                                   // 1e-28 * SolverConfig::tolerance_scale^2

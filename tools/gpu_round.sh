@@ -34,20 +34,20 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
       --no-cpu-baseline --no-flush > "gpurun_out/ncu_${cfg}__${name}.log" 2>&1
     echo "ncu $cfg $name rc=$?"
   }
-  # the split solver at m = 60: per push jacobi_kernel<60,1>, sweep_kernel, jacobi_kernel<60,3>
+  # the split solver at m = 60: per push jacobi_kernel<60,1>, sweep_bip_kernel, jacobi_kernel<60,3>
   cap c3 jacobi_prologue "^jacobi_kernel" 2 8
   cap c3 jacobi_epilogue "^jacobi_kernel" 3 8
-  for K in sweep_kernel spectrum_mma_kernel correlation_kernel stft_kernel integrate_peaks_kernel; do
+  for K in sweep_bip_kernel spectrum_mma_kernel correlation_kernel stft_kernel integrate_peaks_kernel; do
     cap c3 $K "^$K" 1 8
   done
   cap c4 spectrum_tc_kernel "^spectrum_tc_kernel" 1 8
-  cap c1 jacobi_kernel "^jacobi_kernel" 1 4
-  cap c2 jacobi_kernel "^jacobi_kernel" 1 4
+  cap c1 small_jacobi_kernel "^small_jacobi_kernel" 1 4
+  cap c2 small_jacobi_kernel "^small_jacobi_kernel" 1 4
   # summaries on the box (the reports exceed gpurun's 64 MiB copy-back):
   # text per capture, launch shares, per-config DRAM traffic
   python tools/ncu_summary.py r02 gpurun_out/summary > /dev/null 2>&1; echo "ncu summary rc=$?"
   mkdir -p gpurun_out/reps
-  for f in gpurun_out/prof_c3__sweep_kernel gpurun_out/prof_c3__jacobi_epilogue gpurun_out/prof_c4__spectrum_tc_kernel; do
+  for f in gpurun_out/prof_c3__sweep_bip_kernel gpurun_out/prof_c3__jacobi_epilogue gpurun_out/prof_c4__spectrum_tc_kernel; do
     [ -f $f.ncu-rep ] && mv $f.ncu-rep gpurun_out/reps/
   done
   rm -f gpurun_out/prof_*.ncu-rep
