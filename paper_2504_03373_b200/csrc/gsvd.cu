@@ -1711,6 +1711,16 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
 // (gsvd.cpp:642-674); the Gram certificate is run_sweeps'.
 constexpr int kBipRows = 15;  // 60 rows over 4 lanes
 
+// Shared-memory position of column c: columns 4k+2 and 4k+3 trade places.
+// The two processors of a quarter-warp load the tops of adjacent slots, and
+// the tops start as the even columns: at a column stride of 60 x 16 bytes a
+// column's bank half is its parity, so every such pair hit the same 16 banks
+// (2-way conflicts on every top load and store, 400M conflicts per 8-block
+// launch); with the swap adjacent even columns alternate (1.5% of the pairs
+// conflict over a sweep).  W, cn and the Gram certificate all live in
+// position space; the ordering works on column ids.
+__device__ __forceinline__ int bip_pos(int c) { return c ^ ((c >> 1) & 1); }
+
 // the warps of this thread's S-processor group (eight processors per warp)
 __device__ __forceinline__ void bip_group_sync(int S, int warp) {
     if (S >= 32) {
@@ -1735,7 +1745,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
     const int g = tid >> 2, s = tid & 3;  // processor, lane in it
     const long long clk0 = clock64();
     double2* wg = a.wscratch + (size_t)blockIdx.x * m * m;
-    for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
+    for (int e = tid; e < m * m; e += blockDim.x) W[bip_pos(e / m) * m + e % m] = wg[e];
     if (tid == 0) {
         s_rots = 0;
         s_maxrel = 0u;
@@ -1767,8 +1777,8 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
         int qid = 2 * g + 1;  // resident bottom
         double2 Q[R];
 #pragma unroll
-        for (int u = 0; u < R; ++u) Q[u] = qid < m ? W[qid * m + s + 4 * u] : make_double2(0, 0);
-        double cq = cn[qid];
+        for (int u = 0; u < R; ++u) Q[u] = qid < m ? W[bip_pos(qid) * m + s + 4 * u] : make_double2(0, 0);
+        double cq = cn[bip_pos(qid)];
         bool qdirty = false;
         __syncthreads();  // every thread has read s_rots / s_maxrel
         if (tid == 0) {
@@ -1792,14 +1802,14 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
                 if (pid < m && qid < m) {
                     double2 P[R];
 #pragma unroll
-                    for (int u = 0; u < R; ++u) P[u] = W[pid * m + s + 4 * u];
-                    double cp = cn[pid];
+                    for (int u = 0; u < R; ++u) P[u] = W[bip_pos(pid) * m + s + 4 * u];
+                    double cp = cn[bip_pos(pid)];
                     if (rotate_pair<R, 4>(P, Q, cp, cq, 0.0, s, m, mymax, a.tol2)) {
 #pragma unroll
-                        for (int u = 0; u < R; ++u) W[pid * m + s + 4 * u] = P[u];
-                        __syncwarp(group_mask<4>());  // the group's loads of cn[pid] precede the write
+                        for (int u = 0; u < R; ++u) W[bip_pos(pid) * m + s + 4 * u] = P[u];
+                        __syncwarp(group_mask<4>());  // the group's loads of cn[bip_pos(pid)] precede the write
                         if (s == 0) {
-                            cn[pid] = cp;
+                            cn[bip_pos(pid)] = cp;
                             ++myrots;
                         }
                         qdirty = true;
@@ -1823,15 +1833,15 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
                 if (qid < m) {
                     if (qdirty) {
 #pragma unroll
-                        for (int u = 0; u < R; ++u) W[qid * m + s + 4 * u] = Q[u];
+                        for (int u = 0; u < R; ++u) W[bip_pos(qid) * m + s + 4 * u] = Q[u];
                     }
                     __syncwarp(group_mask<4>());
-                    if (s == 0) cn[qid] = cq;
+                    if (s == 0) cn[bip_pos(qid)] = cq;
                 }
                 qdirty = false;
 #pragma unroll
-                for (int u = 0; u < R; ++u) Q[u] = nid < m ? W[nid * m + s + 4 * u] : make_double2(0, 0);
-                cq = cn[nid];
+                for (int u = 0; u < R; ++u) Q[u] = nid < m ? W[bip_pos(nid) * m + s + 4 * u] : make_double2(0, 0);
+                cq = cn[bip_pos(nid)];
                 __syncwarp(group_mask<4>());
                 if (s == 0) slot_id[sl] = qid;
                 qid = nid;
@@ -1845,7 +1855,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
         // the resident bottoms go home
         if (qid < m && qdirty) {
 #pragma unroll
-            for (int u = 0; u < R; ++u) W[qid * m + s + 4 * u] = Q[u];
+            for (int u = 0; u < R; ++u) W[bip_pos(qid) * m + s + 4 * u] = Q[u];
         }
         ++sweep;
         if (s == 0 && myrots) {
@@ -1860,7 +1870,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
         prev_maxrel = s_maxrel != 0u;
     }
     __syncthreads();
-    for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[e];
+    for (int e = tid; e < m * m; e += blockDim.x) wg[e] = W[bip_pos(e / m) * m + e % m];
     if (tid == 0) {
         a.sweeps[blockIdx.x] = (uint32_t)sweep;
         a.conv[blockIdx.x] = converged ? 1 : 0;
