@@ -8,7 +8,8 @@
   corners  generic canonical kernel (refine mode, a tied group above kZMax), rejected picker
            candidates, generic m = 37 and m = 16
   stream   device STFT, sample pushes across calls, async pushes with the result ring, the gate
-  small    the warp solver (m <= 8) incl. worklisted (vanishing / tied) bins
+  small    the lane-group solver (m = 8 and 16) incl. in-group canonicalization of vanishing / tied
+           bins and the refine-mode worklist
   tc       the tcgen05 spectrum (bulk copies, TMEM, mbarriers) with padding and odd m
   er       E_r / residual, inverses (float, pivot-free), PD gate eigenvalues
   formats  noise capture, file loaders into a context, the direct-sum STFT
@@ -136,9 +137,20 @@ def case_small():
     r[2] = np.diag(np.arange(1, 9)).astype(np.complex64)
     eng2 = ssl.Engine(8, 3, window_frames=2, max_batch=2)
     eng2.set_noise_identity()
-    print("small worklist", eng2.gsvd(r)[3].all())
+    print("small canonical groups", eng2.gsvd(r)[3].all())
     eng.close()
     eng2.close()
+    # m = 16 (16-lane groups): a tied pair, a rank-deficient bin, refine mode (worklist)
+    r16 = np.zeros((3, 16, 16), np.complex64)
+    r16[0] = np.diag(np.r_[3.0, 3.0, np.arange(14, 0, -1)]).astype(np.complex64)
+    x16 = rng.standard_normal((16, 5)) + 1j * rng.standard_normal((16, 5))
+    r16[1] = x16 @ x16.conj().T
+    r16[2] = np.diag(np.arange(16, 0, -1)).astype(np.complex64)
+    for refine in (False, True):
+        eng3 = ssl.Engine(16, 3, window_frames=2, max_batch=2, solver=ssl.SolverConfig(refine_leading=refine))
+        eng3.set_noise_identity()
+        print("small m=16 refine", refine, eng3.gsvd(r16)[3].all())
+        eng3.close()
 
 
 def case_tc():
