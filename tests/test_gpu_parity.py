@@ -524,3 +524,46 @@ def test_60ch_solver_paths_against_oracle(port, precondition):
     assert np.all(conv)
     assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
     assert np.max(np.abs(e[0] - want["e"])) <= 1e-6
+
+
+@pytest.mark.parametrize("m", [3, 8, 12, 16])
+@pytest.mark.parametrize("case", ["tied", "rank_deficient", "rejected"])
+def test_lane_group_canonicalization_against_oracle(port, m, case):
+    """The lane-group solver (m <= 16, csrc/small.cu) canonicalizes vanishing
+    blocks and tied groups itself (canonicalize_subspaces, gsvd.cpp:381-565,
+    with the picker of gsvd.cpp:404-436): a run of equal values, a
+    rank-deficient R (vanishing block), and unit vectors inside the kept span
+    (candidates the picker must reject) must all give the oracle's bases."""
+    from paper_2504_03373_b200 import ssl
+
+    bins = 3
+    rng = np.random.default_rng(17 * m + len(case))
+    if case == "tied":
+        d = max(2, m // 2)
+        s = np.concatenate([np.linspace(9.0, 5.0, (m - d + 1) // 2), np.full(d, 2.0),
+                            np.linspace(1.5, 0.5, m - d - (m - d + 1) // 2)])
+        r = np.empty((bins, m, m), np.complex64)
+        for b in range(bins):
+            q, _ = np.linalg.qr(rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m)))
+            r[b] = (q * s) @ q.conj().T
+    else:
+        rank = max(1, m // 2)
+        x = rng.standard_normal((bins, m, rank)) + 1j * rng.standard_normal((bins, m, rank))
+        if case == "rejected" and m >= 3 and rank >= 2:
+            x[:, 0, 2:] = 0
+            x[:, 2 % m, 2:] = 0
+            x[:, :, 0] = 0
+            x[:, :, 1] = 0
+            x[:, 0, 0] = 3.0
+            x[:, 2 % m, 1] = 2.0
+        r = (x @ x.conj().transpose(0, 2, 1) / rank).astype(np.complex64)
+    k = np.broadcast_to(np.eye(m, dtype=np.complex64), (bins, m, m)).copy()
+    eng = ssl.Engine(m, bins, window_frames=2, max_batch=2)
+    eng.set_noise_model(k)
+    sigma, e, _, conv = eng.gsvd(r)
+    eng.close()
+    want = port.gsvd_reference(k, r, threads=4)
+    smax = want["sigma"][:, :1]
+    assert np.all(conv)
+    assert np.max(np.abs(sigma[0] - want["sigma"]) / smax) <= SIGMA_TOL
+    assert np.max(np.abs(e[0] - want["e"])) <= 1e-6, (m, case)
