@@ -83,6 +83,50 @@ __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
 }
 
 
+// Small arrays (m <= 8: C1): one WARP per
+// (block, bin), eight per CTA.  The bin's noise vectors sit in the warp's
+// slice of shared memory (broadcast reads); each lane takes directions
+// lane, lane + 32, ... with its steering vector in registers and runs the
+// noise vectors in order, so every direction runs the identical instruction
+// sequence (exact ties survive) and the denominator sums in the reference's
+// vector order (music.cpp:140-152).  One CTA-wide load of the direction chunk
+// per (block, bin) in spectrum_kernel cost more than the arithmetic at these
+// sizes (C1: 68 us per 32 blocks).
+constexpr int kSpecWarps = 8;
+
+template <int MCAP>
+__global__ void __launch_bounds__(32 * kSpecWarps) spectrum_warp_kernel(SpecArgs a, int nbb) {
+    if (a.abort && *a.abort) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = a.m, nn = m - a.ns;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* En = reinterpret_cast<double2*>(smem_raw) + (size_t)warp * nn * m;
+    const int bb = blockIdx.x * kSpecWarps + warp;  // block * bins + bin
+    if (bb >= nbb) return;                          // a whole warp
+    const int bin = bb % a.bins;
+    const double2* eb = a.e + ((size_t)bb * m + a.ns) * m;
+    for (int x = lane; x < nn * m; x += 32) En[x] = eb[x];
+    __syncwarp();
+    for (int d = lane; d < a.dirs; d += 32) {
+        const float2* hb = a.h + ((size_t)bin * a.dirs + d) * m;
+        double2 h[MCAP];
+#pragma unroll
+        for (int i = 0; i < MCAP; ++i) h[i] = i < m ? f2d(hb[i]) : make_double2(0, 0);
+        double den = 0;
+        for (int v = 0; v < nn; ++v) {
+            const double2* ev = En + v * m;
+            double2 acc = make_double2(0, 0);
+#pragma unroll
+            for (int i = 0; i < MCAP; ++i)
+                if (i < m) acc = cadd(acc, cmulc(h[i], ev[i]));
+            const double mag = hypot(acc.x, acc.y);
+            den += a.squared ? mag * mag : mag;
+        }
+        if (den < a.floor_) den = a.floor_;
+        a.p[(size_t)bb * a.dirs + d] = a.num[(size_t)bin * a.dirs + d] / den;
+    }
+}
+
 // FP64 tensor-core variant (DMMA, mma.sync m8n8k4 .f64), used whenever the
 // noise subspace has 16..64 vectors (C3, C4; C1/C2 keep the kernel above):
 // the contraction
@@ -298,7 +342,22 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
             const int nb = min(cb, a.bins - b0);
             __syncthreads();
             const double* src = pb + (size_t)b0 * a.dirs;
-            for (int x = t; x < nb * a.dirs; x += blockDim.x) stage[x] = src[x];
+            // eight loads in flight per thread (a load-store loop through
+            // generic pointers is serialized: one L2 round trip per element)
+            const int n = nb * a.dirs;
+            for (int x0 = t; x0 < n; x0 += 8 * blockDim.x) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int x = x0 + u * blockDim.x;
+                    v[u] = x < n ? __ldg(src + x) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int x = x0 + u * blockDim.x;
+                    if (x < n) stage[x] = v[u];
+                }
+            }
             __syncthreads();
             for (int d = t; d < a.dirs; d += blockDim.x) {
                 double acc = pw[d];
@@ -401,6 +460,13 @@ void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
         };
         if (a.dirs % 72 == 0) mma(spectrum_mma_kernel<9>, 9);
         else mma(spectrum_mma_kernel<8>, 8);
+        return;
+    }
+    if (a.m <= 8) {  // the smallest arrays: a warp per (block, bin) (C2's m = 16 measured slower: 170 vs 133 us)
+        const int nbb = nblk * a.bins;
+        const size_t smemw = (size_t)kSpecWarps * (a.m - a.ns) * a.m * sizeof(double2);
+        cudaFuncSetAttribute(spectrum_warp_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemw);
+        spectrum_warp_kernel<8><<<(nbb + kSpecWarps - 1) / kSpecWarps, 32 * kSpecWarps, smemw, s>>>(a, nbb);
         return;
     }
     size_t smem;
