@@ -86,6 +86,26 @@ __device__ __forceinline__ double2 group_sum2(double2 v) {
     return v;
 }
 
+// store(e, src[e]) for e = t, t + nt, ... < n with B loads in flight per
+// thread: a plain load-store loop through generic pointers is compiled as one
+// dependent global round trip per element (the store may alias the next load)
+template <int B, class T, class F>
+__device__ __forceinline__ void batched_copy(int t, int nt, int n, const T* __restrict__ src, F store) {
+    for (int e0 = t; e0 < n; e0 += B * nt) {
+        T v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int e = e0 + u * nt;
+            if (e < n) v[u] = src[e];
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int e = e0 + u * nt;
+            if (e < n) store(e, v[u]);
+        }
+    }
+}
+
 // block-wide helpers -------------------------------------------------------
 
 // Round-robin (circle method) pairing for an even number of columns n:

@@ -1426,7 +1426,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     }
     if constexpr (PART == 3) {
         const double2* wg = a.wscratch + (size_t)blk * m * m;
-        for (int e = tid; e < m * m; e += blockDim.x) W[e] = wg[e];
+        batched_copy<4>(tid, (int)blockDim.x, m * m, wg, [&](int e, double2 v) { W[e] = v; });
         if (tid < m) qs.piv[tid] = a.pivs[(size_t)blk * kMaxM + tid];
         sweep = (int)a.sweeps[blk];
         converged = a.conv[blk] != 0;
@@ -1745,7 +1745,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
     const int g = tid >> 2, s = tid & 3;  // processor, lane in it
     const long long clk0 = clock64();
     double2* wg = a.wscratch + (size_t)blockIdx.x * m * m;
-    for (int e = tid; e < m * m; e += blockDim.x) W[bip_pos(e / m) * m + e % m] = wg[e];
+    batched_copy<4>(tid, (int)blockDim.x, m * m, wg, [&](int e, double2 v) { W[bip_pos(e / m) * m + e % m] = v; });
     if (tid == 0) {
         s_rots = 0;
         s_maxrel = 0u;

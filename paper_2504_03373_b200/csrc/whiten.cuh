@@ -151,10 +151,8 @@ template <int NT>
 __device__ __forceinline__ void form_whitened_mma(const float2* __restrict__ rb, const double2* __restrict__ kb,
                                                   int m, double2* W, float2* stage, double2* ag) {
     const int t = threadIdx.x;
-    for (int e = t; e < m * m; e += NT) {
-        W[e] = kb[e];
-        stage[e] = rb[e];
-    }
+    batched_copy<4>(t, NT, m * m, kb, [&](int e, double2 v) { W[e] = v; });
+    batched_copy<4>(t, NT, m * m, rb, [&](int e, float2 v) { stage[e] = v; });
     __syncthreads();
     const int warp = t >> 5, lane = t & 31, r = lane >> 2, c = lane & 3;
     const int nt8 = (m + 7) >> 3;
