@@ -342,18 +342,18 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
             const int nb = min(cb, a.bins - b0);
             __syncthreads();
             const double* src = pb + (size_t)b0 * a.dirs;
-            // eight loads in flight per thread (a load-store loop through
+            // sixteen loads in flight per thread (a load-store loop through
             // generic pointers is serialized: one L2 round trip per element)
             const int n = nb * a.dirs;
-            for (int x0 = t; x0 < n; x0 += 8 * blockDim.x) {
-                double v[8];
+            for (int x0 = t; x0 < n; x0 += 16 * blockDim.x) {
+                double v[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const int x = x0 + u * blockDim.x;
                     v[u] = x < n ? __ldg(src + x) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const int x = x0 + u * blockDim.x;
                     if (x < n) stage[x] = v[u];
                 }
@@ -413,7 +413,11 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
         int nb = 0;
         const int cap = a.ns < 64 ? a.ns : 64;
         for (int d = 0; d < a.dirs; ++d) {
-            if (!is_peak[d]) continue;
+            if (!is_peak[d]) {  // skip a run of non-peaks 4 flags at a time
+                if ((d & 3) == 0 && d + 4 <= a.dirs && !(is_peak[d] | is_peak[d + 1] | is_peak[d + 2] | is_peak[d + 3]))
+                    d += 3;
+                continue;
+            }
             const double v = pw[d];
             int pos = nb;
             while (pos > 0 && v > pw[best[pos - 1]]) --pos;
@@ -483,8 +487,10 @@ void launch_steering_prep(const float2* h_in, float2* h_t, double* num, int m, i
 }
 
 void launch_peaks(PeakArgs a, int nblk, cudaStream_t s) {
-    // small grids stage ~40 KB of P per pass (>= 16 bins); large ones read directly
-    a.peak_chunk = (int)(40960 / ((size_t)a.dirs * sizeof(double)));
+    // small grids stage up to 160 KB of P per pass (the whole block at D = 72:
+    // one memory latency instead of four), in chunks of >= 16 bins; large
+    // grids read directly
+    a.peak_chunk = (int)(163840 / ((size_t)a.dirs * sizeof(double)));
     if (a.peak_chunk < 16) a.peak_chunk = 1;
     if (a.peak_chunk > a.bins) a.peak_chunk = a.bins;
     const size_t smem = (size_t)a.dirs * sizeof(double) + (size_t)(a.dirs + (a.dirs & 1)) * sizeof(int) +
