@@ -40,7 +40,12 @@ __device__ __forceinline__ void outer_acc(double2& acc, float2 xi, float2 xj, bo
     }
 }
 
-__global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a) {
+// NT threads own up to PER entries each: 512 x 8 for the full m <= 64, and
+// for small arrays just enough warps to cover the m x m entries once (C1:
+// 64 threads; the 512-thread form spent 87% of its issue slots on warps
+// that own no entry).
+template <int NT, int PER>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 2 : 1) correlation_kernel(CorrArgs a) {
     if (a.abort && *a.abort) return;  // skipped after a failed asynchronous gate
     __shared__ float2 xs_new[kMaxM];
     __shared__ float2 xc_new[kCorrChunk * kMaxM];
@@ -50,11 +55,11 @@ __global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a
     const int mm = m * m;
     const int tid = threadIdx.x;
 
-    double2 acc[kCorrPer];
-    int eij[kCorrPer];  // (row << 8) | column of each owned entry
+    double2 acc[PER];
+    int eij[PER];  // (row << 8) | column of each owned entry
 #pragma unroll
-    for (int k = 0; k < kCorrPer; ++k) {
-        const int e = tid + k * kCorrThreads;
+    for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * NT;
         eij[k] = ((e / m) << 8) | (e % m);
         acc[k] = e < mm ? a.state[(size_t)b * mm + e] : make_double2(0, 0);
     }
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a
     for (int f0 = 0; f0 < a.frames; f0 += kCorrChunk) {
         const int nf = min(kCorrChunk, a.frames - f0);
         __syncthreads();
-        for (int x = tid; x < nf * m; x += kCorrThreads) {
+        for (int x = tid; x < nf * m; x += NT) {
             const int fi = x / m, ch = x - fi * m;
             const long long g = a.pushed0 + f0 + fi;
             xc_new[x] = frame_ptr(g)[(size_t)ch * a.bins + b];
@@ -85,8 +90,8 @@ __global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a
             const float2* xn = xc_new + fi * m;
             const float2* xo = xc_old + fi * m;
 #pragma unroll
-            for (int k = 0; k < kCorrPer; ++k) {
-                if (tid + k * kCorrThreads < mm) {
+            for (int k = 0; k < PER; ++k) {
+                if (tid + k * NT < mm) {
                     if (drop_old) outer_acc(acc[k], xo[eij[k] >> 8], xo[eij[k] & 255], true);
                     outer_acc(acc[k], xn[eij[k] >> 8], xn[eij[k] & 255], false);
                 }
@@ -96,23 +101,23 @@ __global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a
                 // rebuild oldest first (correlation.cpp:75-84)
                 const long long have = pushed < a.t ? pushed : a.t;
 #pragma unroll
-                for (int k = 0; k < kCorrPer; ++k) acc[k] = make_double2(0, 0);
+                for (int k = 0; k < PER; ++k) acc[k] = make_double2(0, 0);
                 for (long long kk = 0; kk < have; ++kk) {
                     const long long gg = pushed - have + kk;
                     __syncthreads();
                     if (tid < m) xs_new[tid] = frame_ptr(gg)[(size_t)tid * a.bins + b];
                     __syncthreads();
 #pragma unroll
-                    for (int k = 0; k < kCorrPer; ++k)
-                        if (tid + k * kCorrThreads < mm) outer_acc(acc[k], xs_new[eij[k] >> 8], xs_new[eij[k] & 255], false);
+                    for (int k = 0; k < PER; ++k)
+                        if (tid + k * NT < mm) outer_acc(acc[k], xs_new[eij[k] >> 8], xs_new[eij[k] & 255], false);
                 }
                 since = 0;
             }
             if (f >= first_emit) {
                 float2* r = a.r_out + ((size_t)(f - first_emit) * a.bins + b) * mm;
 #pragma unroll
-                for (int k = 0; k < kCorrPer; ++k) {
-                    const int e = tid + k * kCorrThreads;
+                for (int k = 0; k < PER; ++k) {
+                    const int e = tid + k * NT;
                     if (e < mm)
                         r[e] = make_float2(__double2float_rn(__dmul_rn(acc[k].x, inv_t)),
                                            __double2float_rn(__dmul_rn(acc[k].y, inv_t)));
@@ -121,8 +126,8 @@ __global__ void __launch_bounds__(kCorrThreads, 2) correlation_kernel(CorrArgs a
         }
     }
 #pragma unroll
-    for (int k = 0; k < kCorrPer; ++k) {
-        const int e = tid + k * kCorrThreads;
+    for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * NT;
         if (e < mm) a.state[(size_t)b * mm + e] = acc[k];
     }
 }
@@ -154,7 +159,14 @@ void launch_gate_abort(const float* p, size_t n, unsigned int* abort, unsigned i
 }
 
 void launch_correlation(const CorrArgs& a, cudaStream_t s) {
-    correlation_kernel<<<a.bins, kCorrThreads, 0, s>>>(a);
+    const int mm = a.m * a.m;
+    if (mm <= 64) {
+        correlation_kernel<64, 1><<<a.bins, 64, 0, s>>>(a);
+    } else if (mm <= 256) {
+        correlation_kernel<256, 1><<<a.bins, 256, 0, s>>>(a);
+    } else {
+        correlation_kernel<kCorrThreads, kCorrPer><<<a.bins, kCorrThreads, 0, s>>>(a);
+    }
 }
 
 void launch_count_nonfinite(const float* p, size_t n, unsigned int* bad, cudaStream_t s) {
