@@ -366,16 +366,16 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
             }
         }
     } else {
-        // large grids: a thread per direction, 16 bins' loads in flight
+        // large grids: a thread per direction, 32 bins' loads in flight
         for (int d = t; d < a.dirs; d += blockDim.x) {
             double acc = 0.0;
             int b = 0;
-            for (; b + 16 <= a.bins; b += 16) {
-                double v[16];
+            for (; b + 32 <= a.bins; b += 32) {
+                double v[32];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) v[u] = pb[(size_t)(b + u) * a.dirs + d];
+                for (int u = 0; u < 32; ++u) v[u] = __ldg(pb + (size_t)(b + u) * a.dirs + d);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, v[u]);
+                for (int u = 0; u < 32; ++u) acc = __dadd_rn(acc, v[u]);
             }
             for (; b < a.bins; ++b) acc = __dadd_rn(acc, pb[(size_t)b * a.dirs + d]);
             pw[d] = acc;
@@ -406,18 +406,19 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
         is_peak[d] = ok;
     }
     __syncthreads();
-    if (t == 0) {
+    if (t < 32) {
         // insertion into a bounded list ordered by (power desc, index asc);
-        // peaks are visited in index order, so equal powers keep index order
+        // peaks are visited in index order, so equal powers keep index order.
+        // Warp 0 finds the peak directions 32 at a time by ballot; lane 0
+        // inserts them.
         uint32_t best[64];
         int nb = 0;
         const int cap = a.ns < 64 ? a.ns : 64;
-        for (int d = 0; d < a.dirs; ++d) {
-            if (!is_peak[d]) {  // skip a run of non-peaks 4 flags at a time
-                if ((d & 3) == 0 && d + 4 <= a.dirs && !(is_peak[d] | is_peak[d + 1] | is_peak[d + 2] | is_peak[d + 3]))
-                    d += 3;
-                continue;
-            }
+        for (int d0 = 0; d0 < a.dirs; d0 += 32) {
+            unsigned bal = __ballot_sync(0xffffffffu, d0 + t < a.dirs && is_peak[d0 + t]);
+            if (t != 0) continue;
+            for (; bal; bal &= bal - 1) {
+            const int d = d0 + __ffs(bal) - 1;
             const double v = pw[d];
             int pos = nb;
             while (pos > 0 && v > pw[best[pos - 1]]) --pos;
@@ -426,7 +427,9 @@ __global__ void __launch_bounds__(kPeakThreads) integrate_peaks_kernel(PeakArgs 
             for (int k = last; k > pos; --k) best[k] = best[k - 1];
             best[pos] = (uint32_t)d;
             if (nb < cap) ++nb;
+            }
         }
+        if (t != 0) return;
         const double thr = a.low_ratio * s_mean;
         for (int k = 0; k < nb; ++k) {
             a.est_idx[(size_t)blk * a.ns + k] = best[k];

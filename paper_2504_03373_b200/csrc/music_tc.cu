@@ -325,14 +325,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) spectrum_tc_kernel(SpecArgs a, 
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 const int j0 = 32 * half + c0 / 2;  // first noise vector of this load
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < 8; q += 2) {
                     // h^H e = main + correction; |.| in FP32 (the products carry
-                    // ~1e-7 already), summed in FP64
-                    const float re = __uint_as_float(v[2 * q]) + __uint_as_float(w[2 * q]);
-                    const float im = __uint_as_float(v[2 * q + 1]) + __uint_as_float(w[2 * q + 1]);
-                    const float s2 = fmaf(re, re, im * im);
-                    const float mag = a.squared ? s2 : sqrtf(s2);
-                    dp[q & 3] += j0 + q < nn ? (double)mag : 0.0;
+                    // ~1e-7 already); two magnitudes added in FP32 (one more
+                    // 2^-24 relative rounding) before each FP64 accumulation:
+                    // the FP64 pipe is this epilogue's throttle
+                    float mg[2];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const float re = __uint_as_float(v[2 * (q + r)]) + __uint_as_float(w[2 * (q + r)]);
+                        const float im = __uint_as_float(v[2 * (q + r) + 1]) + __uint_as_float(w[2 * (q + r) + 1]);
+                        const float s2 = fmaf(re, re, im * im);
+                        const float mag = a.squared ? s2 : sqrtf(s2);
+                        mg[r] = j0 + q + r < nn ? mag : 0.0f;
+                    }
+                    dp[q >> 1] += (double)(mg[0] + mg[1]);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
