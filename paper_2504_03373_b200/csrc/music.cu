@@ -21,6 +21,12 @@
 namespace sslg {
 
 constexpr int kSpecThreads = 256;
+
+// |z| as sqrt(x^2 + y^2): the projections are far from the overflow and
+// underflow ranges hypot guards against, and its guarded sequence was a large
+// share of the spectrum's FP64 work; every direction still runs the identical
+// instruction sequence (exact ties survive)
+__device__ __forceinline__ double cabs_fast(double2 z) { return sqrt(fma(z.x, z.x, z.y * z.y)); }
 constexpr int kSpecVec = 4;  // noise vectors per steering load
 
 __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
@@ -65,7 +71,7 @@ __global__ void __launch_bounds__(kSpecThreads) spectrum_kernel(SpecArgs a) {
 #pragma unroll
             for (int u = 0; u < kSpecVec; ++u) {
                 if (v0 + u < nn) {
-                    const double mag = hypot(acc[u].x, acc[u].y);
+                    const double mag = cabs_fast(acc[u]);
                     den += a.squared ? mag * mag : mag;
                 }
             }
@@ -119,7 +125,7 @@ __global__ void __launch_bounds__(32 * kSpecWarps) spectrum_warp_kernel(SpecArgs
 #pragma unroll
             for (int i = 0; i < MCAP; ++i)
                 if (i < m) acc = cadd(acc, cmulc(h[i], ev[i]));
-            const double mag = hypot(acc.x, acc.y);
+            const double mag = cabs_fast(acc);
             den += a.squared ? mag * mag : mag;
         }
         if (den < a.floor_) den = a.floor_;
