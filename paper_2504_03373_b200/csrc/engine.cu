@@ -244,7 +244,9 @@ int run_gsvd(sslg_ctx* c, int n) {
     c->launches += launch_jacobi(ga, n, c->stream);
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
-    if (g.canonical_subspaces) {
+    // the lane-group solver (m <= 16) canonicalizes every bin itself unless
+    // refine mode asks for the full-space A A^H refinement: no worklist pass
+    if (g.canonical_subspaces && !(small_jacobi_selected(ga) && !g.refine_leading)) {
         CanonArgs ca{c->r, c->kinv, c->sigma, c->e, c->work, (int)g.m, (int)g.bins, g.refine_leading};
         ca.abort = c->abort;
         launch_canonical(ca, n, c->stream);

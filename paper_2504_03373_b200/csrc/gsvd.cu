@@ -1894,7 +1894,7 @@ int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
         launch(jacobi_kernel<60, 3>, jac_threads<60>(), 60);
         return 3;
     }
-    if (small_jacobi_supported(a) && !a.phase_clk && !a.force_cta) {  // C1 / C2 sizes: one warp per bin
+    if (small_jacobi_selected(a)) {  // C1 / C2 sizes: a lane group per bin
         launch_small_jacobi(a, nblk, s);
         return 1;
     }

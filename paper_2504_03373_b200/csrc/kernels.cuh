@@ -72,6 +72,9 @@ struct GsvdArgs {
 int launch_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 // m <= 8: one warp per (block, bin) (small.cu)
 bool small_jacobi_supported(const GsvdArgs& a);
+// the lane-group solver will run (launch_jacobi's choice for m <= 16); it
+// canonicalizes every bin itself unless refine mode is on
+bool small_jacobi_selected(const GsvdArgs& a);
 void launch_small_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s);
 
 struct CanonArgs {

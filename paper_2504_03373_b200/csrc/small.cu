@@ -23,9 +23,11 @@
 //      picker (pick_orthonormal, gsvd.cpp:404-436: index order, thresholds
 //      {0.05, 1e-8, 0}, two projection passes against every accepted
 //      vector), lane j owning candidate j; then the phase rule (largest entry
-//      real positive, gsvd.cpp:545-564) on every vector.  Bins that did not
-//      converge, or run with refine_leading (the A A^H refinement), go to
-//      canonical_kernel through the worklist, as from the CTA solver.
+//      real positive, gsvd.cpp:545-564) on every vector (a bin that did not
+//      converge within max_sweeps is canonicalized from its last iterate, as
+//      canonical_kernel would).  Only refine_leading (the A A^H refinement)
+//      sends bins to canonical_kernel through the worklist, so without it the
+//      engine skips that launch.
 //
 // The q column of a pair is stored multiplied by the unit phase ph =
 // a_pq / |a_pq| (Q' ph instead of Q' = s P + c conj(ph) Q), which gives both
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, small_ctas<MC>()) small_jaco
     for (unsigned tl = __ballot_sync(gm, tie) >> base; tl; tl &= tl - 1)
         tie_rank |= 1u << __shfl_sync(gm, rank, base + __ffs(tl) - 1);
     bool special = z > 0 || tie_rank != 0;
-    if (a.canonical && special && !a.refine && converged) {
+    if (a.canonical && special && !a.refine) {
         if (z > 0) {
             // candidates e_j projected twice against every lead vector
             double2 c[MC];
@@ -347,6 +349,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, small_ctas<MC>()) small_jaco
 
 // m <= 16: lane groups of 8 (C1) or 16 (C2) lanes
 bool small_jacobi_supported(const GsvdArgs& a) { return a.m <= 16; }
+bool small_jacobi_selected(const GsvdArgs& a) { return small_jacobi_supported(a) && !a.phase_clk && !a.force_cta; }
 
 void launch_small_jacobi(const GsvdArgs& a, int nblk, cudaStream_t s) {
     const int n = nblk * a.bins;
