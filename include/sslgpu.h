@@ -337,6 +337,9 @@ uint32_t sslg_last_launch_count(const sslg_ctx* ctx);
 /* Measured FP64 FMA throughput of `device` (TFLOP/s): the roofline
  * denominator for the FP64 solver kernels. */
 int sslg_probe_fp64_tflops(int device, double* tflops);
+/* Measured FP32 FMA throughput of `device` (TFLOP/s): the ceiling a float
+ * solver would have (reported beside the FP64 fraction). */
+int sslg_probe_fp32_tflops(int device, double* tflops);
 /* Diagnostics: SM clocks summed over all GSVD CTAs per solver phase
  * (whiten, QR, sweeps, sigma/back-multiply, basis completion, canonical
  * picker + phase, store) since the last reset; needs SSLG_PHASE_CLOCKS=1 in

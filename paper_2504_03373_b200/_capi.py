@@ -105,6 +105,7 @@ EXPORTS = {
     "sslg_last_stage_ms": (C.c_int, [C.c_void_p, _f32p]),
     "sslg_last_launch_count": (C.c_uint32, [C.c_void_p]),
     "sslg_probe_fp64_tflops": (C.c_int, [C.c_int, _f64p]),
+    "sslg_probe_fp32_tflops": (C.c_int, [C.c_int, _f64p]),
     "sslg_debug_phase_clocks": (C.c_int, [C.c_void_p, _f64p, C.c_int]),
     "sslg_stft_config_default": (None, [C.POINTER(StftConfig)]),
     "sslg_set_stft": (C.c_int, [C.c_void_p, C.POINTER(StftConfig)]),
