@@ -1479,56 +1479,93 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
     mark(3);
 
     // ---- canonicalization (gsvd.cpp:470-565) ---------------------------
-    if (tid == 0) {
+    // Structure of the sorted values, by warp 0 with ballots over the ranks
+    // (two 32-rank halves): the vanishing suffix, the tied runs above it,
+    // the re-orthonormalization line and the dropped / certified lists.
+    //
+    // Fused path: the final (rotation-free) sweep certified every pair of
+    // columns above that sweep's drop line orthogonal (its cn[] are the final
+    // squared norms).  Columns at or below the line (sigma <= 1e-10
+    // sigma_max, always in the vanishing block) are completed to an
+    // orthonormal basis below.  In the preconditioned path u_j = A P x_j /
+    // sigma_j carries the Jacobi's residual coupling to larger-sigma vectors
+    // amplified by sigma_k / sigma_j; every vector below kReorth sigma_max
+    // (and the whole vanishing block) is therefore re-orthonormalized, in rank
+    // order, against all larger ones -- which removes exactly those components
+    // (the ones above keep an error <= 1/kReorth x the Jacobi's 1e-14
+    // relative orthogonality, i.e. <= 1e-9).
+    if (tid < kWarp) {
+        const int lane = tid;
         const double smax = s_sig[s_perm[0]] > 0 ? s_sig[s_perm[0]] : 0.0;
         const double gap = 1e-5 * smax;  // kDegenerateGap (gsvd.cpp:381)
-        int z = 0;
-        while (z < m && s_sig[s_perm[m - 1 - z]] <= gap) ++z;
+        double v[2], vn[2];
+        int jj[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rk = lane + 32 * h;
+            jj[h] = rk < m ? s_perm[rk] : 0;
+            v[h] = rk < m ? s_sig[jj[h]] : -1.0;
+            vn[h] = rk + 1 < m ? s_sig[s_perm[rk + 1]] : -1.0;
+        }
+        // vanishing values form a suffix of the ranks
+        const unsigned van0 = __ballot_sync(0xffffffffu, lane < m && v[0] <= gap);
+        const unsigned van1 = __ballot_sync(0xffffffffu, lane + 32 < m && v[1] <= gap);
+        const int z = __popc(van0) + __popc(van1);
         const int lead_end = m - z;
-        int ng = 0, dmax = 0;  // the vanishing block has no size limit (big_vanish)
-        for (int i = 0; i < lead_end;) {
-            int end = i;
-            while (end + 1 < lead_end && s_sig[s_perm[end]] - s_sig[s_perm[end + 1]] <= gap) ++end;
-            if (end > i) {
-                cs.groups[ng][0] = i;
-                cs.groups[ng][1] = end;
-                ++ng;
-                dmax = max(dmax, end - i + 1);
+        // rank rk ties with rk + 1 (both above the vanishing line)
+        const unsigned long long tie =
+            (unsigned long long)__ballot_sync(0xffffffffu, lane + 1 < lead_end && v[0] - vn[0] <= gap) |
+            ((unsigned long long)__ballot_sync(0xffffffffu, lane + 33 < lead_end && v[1] - vn[1] <= gap) << 32);
+        const unsigned long long starts = tie & ~(tie << 1);  // first rank of each tied run
+        const unsigned long long ends = tie & ~(tie >> 1);    // last tied rank of each run (its group ends one later)
+        int dmax = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rk = lane + 32 * h;
+            if (rk < 64 && ((starts >> rk) & 1ull)) {
+                const int gi = __popcll(starts & ((1ull << rk) - 1ull));
+                const int e = __ffsll((long long)(ends >> rk)) - 1 + rk + 1;  // group's last rank
+                cs.groups[gi][0] = rk;
+                cs.groups[gi][1] = e;
+                dmax = max(dmax, e - rk + 1);
             }
-            i = end + 1;
         }
-        // fused path: the final (rotation-free) sweep certified every pair of
-        // columns above that sweep's drop line orthogonal (its cn[] are the
-        // final squared norms).  Columns at or below the line (sigma <=
-        // 1e-10 sigma_max, always in the vanishing block) are completed to an
-        // orthonormal basis below.
-        // In the preconditioned path u_j = A P x_j / sigma_j carries the
-        // Jacobi's residual coupling to larger-sigma vectors amplified by
-        // sigma_k / sigma_j; every vector below kReorth sigma_max (and the
-        // whole vanishing block) is therefore re-orthonormalized, in rank
-        // order, against all larger ones — which removes exactly those
-        // components (the ones above keep an error <= 1/kReorth x the
-        // Jacobi's 1e-14 relative orthogonality, i.e. <= 1e-9).
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        // the re-orthonormalization line: the first lead rank below kReorth sigma_max
         int r0 = lead_end;
-        if (precond)
-            for (int rk = 0; rk < lead_end; ++rk)
-                if (s_sig[s_perm[rk]] < kReorth * smax) {
-                    r0 = rk;
-                    break;
-                }
-        int nd = 0, nc = 0;
-        for (int rk = 0; rk < m; ++rk) {
-            const int j = s_perm[rk];
-            const bool dropped = precond ? (rk >= r0) : !(cn[j] > drop_last);
-            if (dropped) cs.dropped[nd++] = j;
-            else cs.certcols[nc++] = j;
+        if (precond) {
+            const unsigned b0 = __ballot_sync(0xffffffffu, lane < lead_end && v[0] < kReorth * smax);
+            const unsigned b1 = __ballot_sync(0xffffffffu, lane + 32 < lead_end && v[1] < kReorth * smax);
+            if (b0) r0 = __ffs(b0) - 1;
+            else if (b1) r0 = 32 + __ffs(b1) - 1;
         }
-        cs.ndropped = nd;
-        cs.ncert = nc;
-        const bool clean = converged;
-        cs.ngroups = ng;
-        cs.nvanish = z;
-        cs.eligible = a.canonical && !a.refine && clean && dmax <= kZMax && m <= 64;
+        // dropped (rank order) and certified lists, by stable compaction
+        unsigned dropm[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rk = lane + 32 * h;
+            const bool dr = rk < m && (precond ? (rk >= r0) : !(cn[jj[h]] > drop_last));
+            dropm[h] = __ballot_sync(0xffffffffu, dr);
+        }
+        const int nd0 = __popc(dropm[0]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rk = lane + 32 * h;
+            if (rk < m) {
+                const unsigned below = lane ? (dropm[h] & ((1u << lane) - 1u)) : 0u;
+                const int dpos = (h ? nd0 : 0) + __popc(below);
+                if ((dropm[h] >> lane) & 1u) cs.dropped[dpos] = jj[h];
+                else cs.certcols[rk - dpos] = jj[h];
+            }
+        }
+        if (lane == 0) {
+            cs.ndropped = nd0 + __popc(dropm[1]);
+            cs.ncert = m - cs.ndropped;
+            cs.ngroups = __popcll(starts);
+            cs.nvanish = z;
+            cs.eligible = a.canonical && !a.refine && converged && dmax <= kZMax && m <= 64;
+        }
     }
     __syncthreads();
     // the preconditioned vectors are re-orthonormalized whichever kernel
