@@ -1466,11 +1466,10 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
         }
         s_perm[rank] = tid;
     }
-    for (int e = tid; e < m * m; e += blockDim.x) {
-        const int j = e / m;
-        const double nrm = s_sig[j];
-        W[e] = nrm > 0 ? cscale(1.0 / nrm, W[e]) : make_double2(0, 0);
-    }
+    __shared__ double s_inv[kMaxM];  // 1 / sigma_j, one division per column
+    if (tid < m) s_inv[tid] = s_sig[tid] > 0 ? 1.0 / s_sig[tid] : 0.0;
+    __syncthreads();
+    for (int e = tid; e < m * m; e += blockDim.x) W[e] = cscale(s_inv[e / m], W[e]);
     __syncthreads();
     if (precond) {  // left vectors of X -> of A
         if constexpr (PART == 3) back_multiply_mma<jac_threads<MC>()>(W, ag, m, qs, s_sig);
