@@ -1658,22 +1658,27 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
             pick_in_span(W, Y, m, d, z > 0 && gi == 0, cs);
             apply_span<MC>(W, m, d, cs);
         }
-        // phase rule (gsvd.cpp:545-564): warp per vector
-        const int warp = tid / kWarp, lane = tid % kWarp;
-        for (int rk = warp; rk < m; rk += jac_threads<MC>() / kWarp) {
-            const int j = s_perm[rk];
+        // phase rule (gsvd.cpp:545-564): eight lanes per vector, four vectors
+        // per warp; the first entry of largest magnitude sets the phase
+        const int warp = tid / kWarp, lane = tid % kWarp, sl = lane & 7;
+        for (int rk0 = 4 * warp; rk0 < m; rk0 += 4 * (jac_threads<MC>() / kWarp)) {
+            const int rk = rk0 + (lane >> 3);
+            const bool on = rk < m;
+            const int j = on ? s_perm[rk] : 0;
             double best = -1;
             int bi = 0;
-            for (int i = lane; i < m; i += kWarp) {
-                const double2 v = W[j * m + i];
-                const double mg = hypot(v.x, v.y);
-                if (mg > best) {
-                    best = mg;
-                    bi = i;
+            if (on) {
+                for (int i = sl; i < m; i += 8) {
+                    const double2 v = W[j * m + i];
+                    const double mg = hypot(v.x, v.y);
+                    if (mg > best) {
+                        best = mg;
+                        bi = i;
+                    }
                 }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
+            for (int o = 4; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, best, o);
                 const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (ob > best || (ob == best && oi < bi)) {
@@ -1681,7 +1686,7 @@ __global__ void __launch_bounds__(jac_threads<MC>(), jac_ctas<MC>()) jacobi_kern
                     bi = oi;
                 }
             }
-            if (lane == 0) {
+            if (on && sl == 0) {
                 double2 up = make_double2(1.0, 0.0);
                 if (best > 0) {
                     const double2 val = W[j * m + bi];
