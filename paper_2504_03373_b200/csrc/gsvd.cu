@@ -1110,12 +1110,59 @@ __device__ void back_multiply(double2* W, const double2* __restrict__ ag, int m,
     }
 }
 
+// rotate_pair<R, L>'s no-rotation test (jacobi_rot.cuh) for columns a and b
+// in its exact operation order, for both orientations (which column the sweep
+// loads as P is a property of its ordering): lane s of the pair's group sums
+// rows s + L u into two accumulators by the parity of u, and group_sum2 adds
+// the lanes' partials by the xor butterfly.  True iff either orientation
+// would rotate.
+template <int L>
+__device__ bool pair_rotates_exact(const double2* W, int m, int a, int b, double ca, double cb, double tol2) {
+    for (int o = 0; o < 2; ++o) {
+        const double2* P = W + (o ? b : a) * m;
+        const double2* Q = W + (o ? a : b) * m;
+        const double cp = o ? cb : ca, cq = o ? ca : cb;
+        double2 v[L];
+#pragma unroll
+        for (int s = 0; s < L; ++s) {
+            double d0x = 0, d0y = 0, d1x = 0, d1y = 0;
+            for (int u = 0; s + u * L < m; ++u) {
+                const double2 x = P[s + u * L], y = Q[s + u * L];
+                if (u & 1) {
+                    d1x = fma(x.x, y.x, fma(x.y, y.y, d1x));
+                    d1y = fma(x.x, y.y, fma(-x.y, y.x, d1y));
+                } else {
+                    d0x = fma(x.x, y.x, fma(x.y, y.y, d0x));
+                    d0y = fma(x.x, y.y, fma(-x.y, y.x, d0y));
+                }
+            }
+            v[s] = make_double2(d0x + d1x, d0y + d1y);
+        }
+#pragma unroll
+        for (int h = L / 2; h > 0; h >>= 1) {
+            double2 nv[L];
+#pragma unroll
+            for (int s = 0; s < L; ++s) nv[s] = make_double2(v[s].x + v[s ^ h].x, v[s].y + v[s ^ h].y);
+#pragma unroll
+            for (int s = 0; s < L; ++s) v[s] = nv[s];
+        }
+        const double mag2 = fma(v[0].x, v[0].x, v[0].y * v[0].y);
+        if (!(mag2 <= tol2 * cp * cq)) return true;
+    }
+    return false;
+}
+
 // True iff every pair of columns above the drop line satisfies the
 // reference's no-rotation test |x_p^H x_q|^2 <= 1e-28 |x_p|^2 |x_q|^2, i.e.
 // iff the next sweep would rotate nothing (gsvd.cpp:642-649).  Evaluated as
 // one 4x4-register-tiled Gram product over the upper triangle instead of a
-// full verification sweep of round-synchronized pair visits.
-template <int MC, int TS = 2>  // 2x2 tiles keep the fused kernel's register budget
+// full verification sweep of round-synchronized pair visits; a pair the Gram
+// product's summation order puts above the line is re-tested in the order of
+// the sweep it stands in for (L lanes per pair), so a coupling at the 1e-14
+// line does not cost a sweep that would rotate nothing (C3: 7.18 -> 7.14
+// sweeps per bin; most certificates that fail do so for a pair the sweep
+// then rotates).
+template <int MC, int TS = 2, int L = 4>  // 2x2 tiles keep the fused kernel's register budget
 __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, double drop, double tol2) {
     const int m = MC > 0 ? MC : m_rt;
     const int nt = (m + TS - 1) / TS;
@@ -1153,6 +1200,7 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
                     acc[u][v].y = fma(xp[u].x, xq[v].y, fma(-xp[u].y, xq[v].x, acc[u][v].y));
                 }
         }
+        unsigned flagged = 0u;
 #pragma unroll
         for (int u = 0; u < TS; ++u)
 #pragma unroll
@@ -1160,9 +1208,14 @@ __device__ bool gram_converged(const double2* W, int m_rt, const double* cn, dou
                 const int p = p0 + u, q = q0 + v;
                 if (p < q && q < m && cn[p] > drop && cn[q] > drop) {
                     const double mag2 = fma(acc[u][v].x, acc[u][v].x, acc[u][v].y * acc[u][v].y);
-                    if (mag2 > tol2 * cn[p] * cn[q]) bad = true;
+                    if (mag2 > tol2 * cn[p] * cn[q]) flagged |= 1u << (u * TS + v);
                 }
             }
+#pragma unroll 1
+        for (; flagged && !bad; flagged &= flagged - 1) {
+            const int f = __ffs(flagged) - 1, p = p0 + f / TS, q = q0 + f % TS;
+            bad = pair_rotates_exact<L>(W, m, p, q, cn[p], cn[q], tol2);
+        }
     }
     return !__syncthreads_or(bad);
 }
@@ -1289,7 +1342,7 @@ __device__ void run_sweeps(double2* W, int m, double* cn, bool precond, const Gs
         // rotation-free in 98% of bins), or only pairs coupled by <= 1e-8
         // relative, is usually rotation-free: certify that with one Gram
         // product instead of running it (7.44 -> 7.06 sweeps at C3).
-        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC, LPP == 4 ? 4 : 2>(W, m, cn, drop, a.tol2)) {
+        if (sweep > 0 && (2 * prev_rots < total_pairs || prev_maxrel == 0.0) && gram_converged<MC, LPP == 4 ? 4 : 2, LPP>(W, m, cn, drop, a.tol2)) {
             converged = true;
             break;
         }
@@ -1811,7 +1864,7 @@ __global__ void __launch_bounds__(32 * 4, 3) sweep_bip_kernel(GsvdArgs a) {
         __syncthreads();
         // the Gram certificate of a probably rotation-free sweep (see run_sweeps)
         if (sweep > 0 && (2 * prev_rots < total_pairs || !prev_maxrel) &&
-            gram_converged<MC, 4>(W, m, cn, 0.0, a.tol2)) {
+            gram_converged<MC, 4, 4>(W, m, cn, 0.0, a.tol2)) {
             converged = true;
             break;
         }
