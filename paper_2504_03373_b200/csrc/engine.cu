@@ -159,7 +159,7 @@ struct sslg_ctx {
         uint32_t* idx = nullptr;   // pinned [max_batch][ns]
         double* pw = nullptr;      // pinned [max_batch][ns]
         uint8_t* low = nullptr;    // pinned [max_batch][ns]
-        uint32_t* cnt = nullptr;   // pinned [max_batch]
+        uint32_t* cnt = nullptr;   // pinned [max_batch + 1]; cnt[max_batch]: the abort word after this sub-push
         double* power = nullptr;   // pinned [max_batch][dirs] (allocated with the steering)
         uint32_t n = 0;
         long long first_frame = 0;
@@ -428,7 +428,7 @@ int ensure_slots(sslg_ctx* c) {
             cudaMallocHost(&sl.idx, NB * ns * sizeof(uint32_t)) != cudaSuccess ||
             cudaMallocHost(&sl.pw, NB * ns * sizeof(double)) != cudaSuccess ||
             cudaMallocHost(&sl.low, NB * ns) != cudaSuccess ||
-            cudaMallocHost(&sl.cnt, NB * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMallocHost(&sl.cnt, (NB + 1) * sizeof(uint32_t)) != cudaSuccess ||
             (c->dirs && cudaMallocHost(&sl.power, NB * c->dirs * sizeof(double)) != cudaSuccess))
             return set_err(SSLG_DEVICE, "pinned result ring allocation failed");  // sslg_destroy frees the rest
     }
@@ -1526,6 +1526,9 @@ int sslg_push_samples_async(sslg_ctx* c, const float* pcm, uint64_t nsamples, ui
                 CU(cudaMemcpyAsync(sl.power, c->power, (size_t)e * c->dirs * sizeof(double), cudaMemcpyDeviceToHost,
                                    c->stream));
         }
+        // the abort word as of this sub-push, read by sslg_wait_results from
+        // pinned memory after the event (no synchronous copy on that path)
+        CU(cudaMemcpyAsync(sl.cnt + c->cfg.max_batch, c->abort, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
         CU(cudaEventRecord(sl.done, c->stream));
         sl.pending = true;
         ++c->next_id;
@@ -1543,9 +1546,13 @@ int sslg_wait_results(sslg_ctx* c, uint64_t ticket, uint32_t cap_blocks, sslg_bl
     if (ticket > c->next_id) return set_err(SSLG_VALIDATION, "unknown ticket");
     const size_t ns = c->cfg.num_sources, D = c->dirs;
     // wait for the last requested sub-push, then check the abort word once
-    if (ticket > c->collected) CU(cudaEventSynchronize(c->slots[(ticket - 1) % sslg_ctx::kSlots].done));
+    // (its copy taken on the stream right after that sub-push)
     unsigned int ab = 0;
-    CU(cudaMemcpy(&ab, c->abort, sizeof ab, cudaMemcpyDeviceToHost));
+    if (ticket > c->collected) {
+        const auto& last = c->slots[(ticket - 1) % sslg_ctx::kSlots];
+        CU(cudaEventSynchronize(last.done));
+        ab = last.cnt[c->cfg.max_batch];
+    }
     // the whole requested range must fit before any slot is consumed
     {
         uint64_t total = 0;

@@ -314,13 +314,13 @@ class Engine:
         f = frames.shape[0]
         ns = self.music.num_sources
         n_max = f
-        blocks = (_capi.BlockOut * max(n_max, 1))()
+        blocks, bptr = _block_buf(n_max)
         idx = np.zeros((n_max, ns), np.uint32)
         pw = np.zeros((n_max, ns))
         low = np.zeros((n_max, ns), np.uint8)
         power = np.zeros((n_max, self.dirs)) if want_power else None
         em = C.c_uint32()
-        rc = self.L.sslg_push_frames(self.h, f32p(frames), f, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
+        rc = self.L.sslg_push_frames(self.h, f32p(frames), f, bptr, u32p(idx), f64p(pw), u8p(low), f64p(power),
                                      C.byref(em))
         return _blocks_result(rc, em.value, blocks, idx, pw, low, power)
 
@@ -357,13 +357,13 @@ class Engine:
             _capi.check(self.L.sslg_samples_pending(self.h, pcm.shape[1], None, C.byref(nb)))
             cap = nb.value
         ns = self.music.num_sources
-        blocks = (_capi.BlockOut * max(cap, 1))()
+        blocks, bptr = _block_buf(cap)
         idx = np.zeros((cap, ns), np.uint32)
         pw = np.zeros((cap, ns))
         low = np.zeros((cap, ns), np.uint8)
         power = np.zeros((cap, self.dirs)) if want_power else None
         em = C.c_uint32()
-        rc = fn(self.h, f32p(pcm), pcm.shape[1], cap, blocks, u32p(idx), f64p(pw), u8p(low), f64p(power),
+        rc = fn(self.h, f32p(pcm), pcm.shape[1], cap, bptr, u32p(idx), f64p(pw), u8p(low), f64p(power),
                 C.byref(em))
         return _blocks_result(rc, em.value, blocks, idx, pw, low, power)
 
@@ -399,24 +399,28 @@ class Engine:
         wait_results(want_power=True))."""
         _capi.check(self.L.sslg_set_async_power(self.h, int(on)))
 
-    def wait_results(self, ticket: int, cap: int = 4096, want_power: bool = False):
-        """Blocks of every asynchronous push up to `ticket`, in order."""
+    def wait_results(self, ticket: int, cap: Optional[int] = None, want_power: bool = False):
+        """Blocks of every asynchronous push up to `ticket`, in order.  `cap`
+        defaults to what the sub-pushes up to `ticket` can emit (max_batch
+        blocks each)."""
         ns = self.music.num_sources
-        blocks = (_capi.BlockOut * max(cap, 1))()
-        idx = np.zeros((cap, ns), np.uint32)
-        pw = np.zeros((cap, ns))
-        low = np.zeros((cap, ns), np.uint8)
-        power = np.zeros((cap, self.dirs)) if want_power else None
+        if cap is None:
+            cap = max(1, (ticket - getattr(self, "_collected", 0)) * self.max_batch)
+        blocks, bptr = _block_buf(cap)
+        idx = np.empty((cap, ns), np.uint32)
+        pw = np.empty((cap, ns))
+        low = np.empty((cap, ns), np.uint8)
+        power = np.empty((cap, self.dirs)) if want_power else None
         em = C.c_uint32()
         try:
-            _capi.check(self.L.sslg_wait_results(self.h, ticket, cap, blocks, u32p(idx), f64p(pw), u8p(low),
+            _capi.check(self.L.sslg_wait_results(self.h, ticket, cap, bptr, u32p(idx), f64p(pw), u8p(low),
                                                  f64p(power), C.byref(em)))
+            self._collected = max(getattr(self, "_collected", 0), ticket)
         finally:
             self._inflight = [(t, a) for t, a in getattr(self, "_inflight", []) if t > ticket]
         n = em.value
-        return dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
-                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
-                    low=low[:n].astype(bool), power=None if power is None else power[:n])
+        return dict(n=n, frame_index=blocks[:n, 0].copy(), count=blocks[:n, 1].copy(), idx=idx[:n],
+                    power_est=pw[:n], low=low[:n].astype(bool), power=None if power is None else power[:n])
 
     def push_device(self, x_dev_ptr: int, nframes: int) -> int:
         em = C.c_uint32()
@@ -425,7 +429,7 @@ class Engine:
 
     def read_results(self, n: int, power=False, bin_power=False, sigma=False):
         ns = self.music.num_sources
-        blocks = (_capi.BlockOut * max(n, 1))()
+        blocks, bptr = _block_buf(n)
         idx = np.zeros((n, ns), np.uint32)
         pw = np.zeros((n, ns))
         low = np.zeros((n, ns), np.uint8)
@@ -434,10 +438,9 @@ class Engine:
         S = np.zeros((n, self.bins, self.m)) if sigma else None
         sw = np.zeros((n, self.bins), np.uint32)
         cv = np.zeros((n, self.bins), np.uint8)
-        _capi.check(self.L.sslg_read_results(self.h, n, blocks, u32p(idx), f64p(pw), u8p(low), f64p(P), f64p(BP),
+        _capi.check(self.L.sslg_read_results(self.h, n, bptr, u32p(idx), f64p(pw), u8p(low), f64p(P), f64p(BP),
                                              f64p(S), u32p(sw), u8p(cv)))
-        return dict(frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
-                    count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx, power_est=pw,
+        return dict(frame_index=blocks[:n, 0].copy(), count=blocks[:n, 1].copy(), idx=idx, power_est=pw,
                     low=low.astype(bool), power=P, bin_power=BP, sigma=S, sweeps=sw, conv=cv.astype(bool))
 
     def copy_bin_power_device(self, dst_ptr: int, n: int) -> None:
@@ -554,13 +557,19 @@ class Engine:
         return idx, pw, low.astype(bool), cnt
 
 
+def _block_buf(n: int):
+    """sslg_block_out [n] as a numpy (frame_index, count) array and the
+    pointer handed to the C ABI (no per-block ctypes objects)."""
+    a = np.zeros((max(n, 1), 2), np.uint32)
+    return a, a.ctypes.data_as(C.POINTER(_capi.BlockOut))
+
+
 def _blocks_result(rc: int, n: int, blocks, idx, pw, low, power):
     """Per-block results of a push.  On an error the blocks emitted before
     it (the frames before the first non-finite one) travel with the
     exception as `.partial`, so run_locate can sink them first like the
     reference's per-frame loop."""
-    out = dict(n=n, frame_index=np.array([blocks[i].frame_index for i in range(n)], np.uint32),
-               count=np.array([blocks[i].count for i in range(n)], np.uint32), idx=idx[:n], power_est=pw[:n],
+    out = dict(n=n, frame_index=blocks[:n, 0].copy(), count=blocks[:n, 1].copy(), idx=idx[:n], power_est=pw[:n],
                low=low[:n].astype(bool), power=None if power is None else power[:n])
     if rc != _capi.SSLG_OK:
         try:
