@@ -87,15 +87,27 @@ __global__ void dft_kernel(StftArgs a) {
     }
 }
 
-int stft_warps_per_cta(int n) {
-    int w = 16384 / n;  // <= 32 KB of shared memory per CTA
+// Warps (frame-channel transforms) per CTA: up to 8 within 32 KB of shared
+// memory, fewer when the launch has fewer than 8 transforms per SM (C1: 32
+// frames x 8 channels -- one warp per CTA spreads them over the SMs instead
+// of 32 SMs running eight each: 16.9 -> 15.3 us per launch).
+int stft_warps_per_cta(int n, int transforms) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+    }
+    int w = 16384 / n;
     if (w > 8) w = 8;
+    const int spread = transforms / sms;
+    if (w > spread) w = spread;
     if (w < 1) w = 1;
     return w;
 }
 
 void launch_stft(const StftArgs& a, int nframes, cudaStream_t s) {
-    const int wpc = stft_warps_per_cta(a.n);
+    const int wpc = stft_warps_per_cta(a.n, nframes * a.m);
     const size_t smem = (size_t)wpc * a.n * sizeof(float2);
     if (smem > 48 * 1024) cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(nframes, (a.m + wpc - 1) / wpc);
