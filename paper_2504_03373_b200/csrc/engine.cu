@@ -126,6 +126,8 @@ struct sslg_ctx {
     uint32_t* work = nullptr;  // generic-canonicalization worklist
     double2* ascratch = nullptr;  // A copies for the preconditioned back-multiply
     double2* wscratch = nullptr;  // W between the split solver kernels (m = 60)
+    uint32_t* done = nullptr;     // per-(block, bin) sweep-completion epochs of the split solver
+    uint32_t epoch = 0;           // last epoch handed to the split solver
     int* pivs = nullptr;          // QR pivots between them
     long long* phase_clk = nullptr;  // solver phase clocks (SSLG_PHASE_CLOCKS=1)
     double* p = nullptr;
@@ -241,6 +243,9 @@ int run_gsvd(sslg_ctx* c, int n) {
     ga.pivs = c->pivs;
     ga.tol2 = 1e-28 * (double)g.tolerance_scale * (double)g.tolerance_scale;
     ga.force_cta = c->small_cta;
+    ga.done = c->done;
+    if (++c->epoch == 0) c->epoch = 1;  // flags start at 0: never a live epoch
+    ga.epoch = c->epoch;
     c->launches += launch_jacobi(ga, n, c->stream);
     TRY(check_last_launch("jacobi_kernel"));
     CU(cudaEventRecord(c->ev[2], c->stream));
@@ -524,6 +529,8 @@ int sslg_create(sslg_ctx** out, const sslg_config* cfg) {
     if (g.precondition) rc |= dalloc(&c->ascratch, NB * B * mm);
     if (g.precondition && g.m == 60 && !std::getenv("SSLG_FUSED_SOLVER")) {
         rc |= dalloc(&c->wscratch, NB * B * mm);
+        rc |= dalloc(&c->done, NB * B);
+        if (!rc) cudaMemset(c->done, 0, NB * B * sizeof(uint32_t));
         rc |= dalloc(&c->pivs, NB * B * 64);
     }
     if (const char* tc = std::getenv("SSLG_SPECTRUM_TC")) c->spectrum_tc = tc[0] == '1' ? 1 : 0;
@@ -557,7 +564,7 @@ void sslg_destroy(sslg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->k,      c->kinv,  c->h_raw, c->h_t,   c->num,     c->nbr_off, c->nbr,
                     c->ring,   c->state, c->r,     c->sigma, c->e,       c->e_tmp,   c->sweeps,
-                    c->conv,   c->work, c->ascratch, c->wscratch, c->pivs, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
+                    c->conv,   c->work, c->ascratch, c->wscratch, c->done, c->pivs, c->phase_clk, c->p,     c->power, c->est_idx, c->est_pw, c->est_low, c->est_count,
                     c->flags};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -66,6 +66,8 @@ struct GsvdArgs {
     int force_cta = 0;            // m <= 8: use the CTA solver instead of the warp solver (A/B, SSLG_SMALL_CTA=1)
     double tol2 = 1e-28;          // no-rotation test |a_pq|^2 <= tol2 |w_p|^2 |w_q|^2 (gsvd.cpp:648);
                                   // 1e-28 * SolverConfig::tolerance_scale^2
+    uint32_t* done = nullptr;     // [nblk][bins] split solver: the launch epoch once a bin's sweeps are stored
+    uint32_t epoch = 0;           // this launch's epoch (nonzero, new per launch)
 };
 // returns the number of kernels launched (1, or 3 when the solver is split
 // around a 128-thread sweep kernel)
