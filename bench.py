@@ -403,12 +403,11 @@ def main():
     value = emitted_all / (total_ms * 1e-3)
     res = eng.read_results(args.batch, sigma=False)
     hits = float(np.mean([set(r[: c].tolist()) == set(w.targets) for r, c in zip(res["idx"], res["count"])]))
-    # azimuth-only match: a planar (circular) array cannot tell +el from -el,
-    # so on the 3D grid (C4) a peak at the target's azimuth but another
-    # elevation row is a correct azimuth estimate
-    taz = sorted(float(w.dirs[t][0]) for t in w.targets)
-    az_hits = float(np.mean([sorted(float(w.dirs[j][0]) for j in r[: c].tolist()) == taz
-                             for r, c in zip(res["idx"], res["count"])]))
+    # fraction of the targets among each block's peaks (on the C4 3D grid
+    # the reference's own peak search ranks an elevation sidelobe of one
+    # target, 10 deg off -- outside the neighbour test -- above another target)
+    recall = float(np.mean([len(set(r[: c].tolist()) & set(w.targets)) / len(w.targets)
+                            for r, c in zip(res["idx"], res["count"])]))
 
     # single-block GSVD latency (one array, one block per launch)
     lat = []
@@ -553,7 +552,7 @@ def main():
             "gsvd_latency_us_single_block": gsvd_latency_us,
             "x_realtime": value / REALTIME_BLOCKS_PER_S,
             "target_hit_rate": hits,
-            "target_azimuth_hit_rate": az_hits,
+            "target_recall": recall,
             "roofline": roofline,
             "kernels": kernels,
             "cpu_baseline": cpu,
