@@ -104,3 +104,28 @@ def test_run_locate_sinks_blocks_before_the_bad_frame(golden):
     for b, fe in enumerate(seen):
         c = int(g["count"][b])
         assert [e.direction_index for e in fe.estimates] == list(g["idx"][b][:c])
+
+
+def test_peak_search_context_never_serves_a_spectrum():
+    """calc_average_power after peak_search at m = num_sources + 1, one bin:
+    the peak-search context holds placeholder steering vectors, so the
+    spectrum must come from its own context (same result before and after)."""
+    from paper_2504_03373_b200 import ssl
+
+    rng = np.random.default_rng(5)
+    m, ns, d = 3, 2, 12
+    x = (rng.standard_normal((6, m)) + 1j * rng.standard_normal((6, m))).astype(np.complex64)
+    r = ssl.CorrelationSet(m, (x.T @ x.conj() / 6).astype(np.complex64)[None])
+    noise = ssl.NoiseModel.identity(m, 1)
+    basis = ssl.gsvd(noise, r)
+    dirs = np.array([[30.0 * i, 0.0] for i in range(d)])
+    h = (rng.standard_normal((d, 1, m)) + 1j * rng.standard_normal((d, 1, m))).astype(np.complex64)
+    steer = ssl.SteeringField(m, 0, 0, dirs, h)
+    cfg = ssl.MusicConfig(num_sources=ns)
+    p1 = ssl.calc_average_power(basis, steer, cfg).power.copy()
+    topo = ssl.DirectionTopology.build(dirs)
+    peaks = ssl.peak_search(p1, dirs, topo, cfg)
+    assert 0 < len(peaks) <= ns
+    p2 = ssl.calc_average_power(basis, steer, cfg).power
+    assert np.array_equal(p1, p2)
+    assert np.all(p1 > 0)
