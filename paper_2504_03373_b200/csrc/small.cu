@@ -62,38 +62,40 @@ __device__ __forceinline__ int lane_of_rank(unsigned gm, int base, int rank, int
     return __ffs(__ballot_sync(gm, rank == r) >> base) - 1;
 }
 
-// c -= (v^H c) v, twice, v = vec of lane src broadcast row by row; every lane
-// of the group takes part in the shuffles, only `active` lanes update c
+// c -= (v^H c) v, twice, v a vector staged in shared memory (broadcast
+// reads); only `active` lanes update c
 template <int MC>
-__device__ __forceinline__ void project_out(double2 (&c)[MC], const double2 (&vec)[MC], unsigned gm, int src,
-                                            bool active) {
+__device__ __forceinline__ void project_out(double2 (&c)[MC], const double2* v, bool active) {
     for (int pass = 0; pass < 2; ++pass) {
         double dx = 0, dy = 0;
 #pragma unroll
         for (int i = 0; i < MC; ++i) {
-            const double vx = __shfl_sync(gm, vec[i].x, src), vy = __shfl_sync(gm, vec[i].y, src);
-            dx = fma(vx, c[i].x, fma(vy, c[i].y, dx));
-            dy = fma(vx, c[i].y, fma(-vy, c[i].x, dy));
+            const double2 vv = v[i];
+            dx = fma(vv.x, c[i].x, fma(vv.y, c[i].y, dx));
+            dy = fma(vv.x, c[i].y, fma(-vv.y, c[i].x, dy));
         }
+        if (active) {
 #pragma unroll
-        for (int i = 0; i < MC; ++i) {
-            const double vx = __shfl_sync(gm, vec[i].x, src), vy = __shfl_sync(gm, vec[i].y, src);
-            if (active) {
-                c[i].x -= fma(dx, vx, -dy * vy);
-                c[i].y -= fma(dx, vy, dy * vx);
+            for (int i = 0; i < MC; ++i) {
+                const double2 vv = v[i];
+                c[i].x -= fma(dx, vv.x, -dy * vv.y);
+                c[i].y -= fma(dx, vv.y, dy * vv.x);
             }
         }
     }
 }
 
 // The reference's picker (pick_orthonormal) over the candidates c (lane j:
-// the image of e_j), right-looking: an accepted candidate is normalized and
-// broadcast, the lane holding rank i0 + taken takes it as its vector, and
-// every remaining candidate is projected against it twice.  Slots left
-// unfilled get zero vectors (the reference's zero-initialized output).
+// the image of e_j), right-looking: an accepted candidate is normalized,
+// staged in sq for the projections, and stored as the vector of rank
+// i0 + taken in the row sv[lane of that rank] (that lane's snapshot belongs to
+// this group and is not read again); every remaining candidate is projected
+// against it twice.  Slots left unfilled get zero vectors (the reference's
+// zero-initialized output); the caller reloads every lane's vector from its
+// row once all groups are picked.
 template <int MC>
-__device__ __forceinline__ void pick_group(double2 (&c)[MC], double2 (&u)[MC], double n0, int i0, int need, int m,
-                                           int j, int rank, unsigned gm, int base) {
+__device__ __forceinline__ void pick_group(double2 (&c)[MC], double2 (*sv)[MC], double2* sq, double n0, int i0,
+                                           int need, int m, int j, int rank, unsigned gm, int base) {
     bool used = j >= m;
     int taken = 0;
     const double thresholds[3] = {0.05, 1e-8, 0.0};
@@ -109,27 +111,28 @@ __device__ __forceinline__ void pick_group(double2 (&c)[MC], double2 (&u)[MC], d
             const unsigned bal = __ballot_sync(gm, ok) >> base;
             if (!bal) break;
             const int sel = __ffs(bal) - 1;
+            const int dl = lane_of_rank(gm, base, rank, i0 + taken);
             if (j == sel) {
                 used = true;
                 const double inv = 1.0 / nr;
 #pragma unroll
-                for (int i = 0; i < MC; ++i) c[i] = cscale(inv, c[i]);
+                for (int i = 0; i < MC; ++i) {
+                    c[i] = cscale(inv, c[i]);
+                    sq[i] = c[i];
+                    sv[dl][i] = c[i];
+                }
             }
-            const bool dst = rank == i0 + taken;  // the accepted vector becomes rank i0 + taken
-#pragma unroll
-            for (int i = 0; i < MC; ++i) {
-                const double qx = __shfl_sync(gm, c[i].x, base + sel), qy = __shfl_sync(gm, c[i].y, base + sel);
-                if (dst) u[i] = make_double2(qx, qy);
-            }
-            project_out<MC>(c, c, gm, base + sel, !used);
+            __syncwarp(gm);
+            project_out<MC>(c, sq, !used);
+            __syncwarp(gm);  // every lane has read sq before the next accepted vector
             start = sel + 1;
             ++taken;
         }
     }
-    for (; taken < need; ++taken)
-        if (rank == i0 + taken)
+    if (rank >= i0 + taken && rank < i0 + need)
 #pragma unroll
-            for (int i = 0; i < MC; ++i) u[i] = make_double2(0, 0);
+        for (int i = 0; i < MC; ++i) sv[j][i] = make_double2(0, 0);
+    __syncwarp(gm);
 }
 
 }  // namespace
@@ -273,13 +276,22 @@ __global__ void __launch_bounds__(32 * kSmallWarps, small_ctas<MC>()) small_jaco
         tie_rank |= 1u << __shfl_sync(gm, rank, base + __ffs(tl) - 1);
     bool special = z > 0 || tie_rank != 0;
     if (a.canonical && special && !a.refine) {
+        // the group's vectors (by lane) and one accepted-vector slot in shared
+        // memory: the projections and candidate sums read them by broadcast
+        __shared__ double2 s_vec[kSmallWarps * kBins][MC][MC];
+        __shared__ double2 s_acc[kSmallWarps * kBins][MC];
+        const int gsl = (threadIdx.x >> 5) * kBins + slot;
+        double2(*sv)[MC] = s_vec[gsl];
+#pragma unroll
+        for (int i = 0; i < MC; ++i) sv[j][i] = w[i];
+        __syncwarp(gm);
         if (z > 0) {
             // candidates e_j projected twice against every lead vector
             double2 c[MC];
 #pragma unroll
             for (int i = 0; i < MC; ++i) c[i] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-            for (int k = 0; k < lead; ++k) project_out<MC>(c, w, gm, base + lane_of_rank(gm, base, rank, k), true);
-            pick_group<MC>(c, w, 1.0, lead, z, m, j, rank, gm, base);
+            for (int k = 0; k < lead; ++k) project_out<MC>(c, sv[lane_of_rank(gm, base, rank, k)], true);
+            pick_group<MC>(c, sv, s_acc[gsl], 1.0, lead, z, m, j, rank, gm, base);
         }
         // tied runs in rank order: ranks i0 .. i1 with bits i0 .. i1-1 set
         for (unsigned rest = tie_rank; rest;) {
@@ -293,24 +305,20 @@ __global__ void __launch_bounds__(32 * kSmallWarps, small_ctas<MC>()) small_jaco
 #pragma unroll
             for (int i = 0; i < MC; ++i) c[i] = make_double2(0, 0);
             for (int k = i0; k <= i1; ++k) {
-                const int src = base + lane_of_rank(gm, base, rank, k);
-                double2 ukj = make_double2(0, 0);
+                // the group's vectors above the vanishing block are unchanged
+                // since the snapshot (the pickers only rewrite their own ranks)
+                const double2* uk = sv[lane_of_rank(gm, base, rank, k)];
+                const double2 ukj = make_double2(uk[j].x, -uk[j].y);  // conj(u_k[j])
 #pragma unroll
-                for (int i = 0; i < MC; ++i) {
-                    const double vx = __shfl_sync(gm, w[i].x, src), vy = __shfl_sync(gm, w[i].y, src);
-                    if (i == j) ukj = make_double2(vx, -vy);  // conj(u_k[j])
-                }
-#pragma unroll
-                for (int i = 0; i < MC; ++i) {
-                    const double vx = __shfl_sync(gm, w[i].x, src), vy = __shfl_sync(gm, w[i].y, src);
-                    c[i] = cadd(c[i], cmul(make_double2(vx, vy), ukj));
-                }
+                for (int i = 0; i < MC; ++i) c[i] = cadd(c[i], cmul(uk[i], ukj));
             }
             double n2 = 0;
 #pragma unroll
             for (int i = 0; i < MC; ++i) n2 = fma(c[i].x, c[i].x, fma(c[i].y, c[i].y, n2));
-            pick_group<MC>(c, w, sqrt(n2), i0, d, m, j, rank, gm, base);
+            pick_group<MC>(c, sv, s_acc[gsl], sqrt(n2), i0, d, m, j, rank, gm, base);
         }
+#pragma unroll
+        for (int i = 0; i < MC; ++i) w[i] = sv[j][i];  // picked vectors, or the snapshot
         special = false;
     }
     const bool phase = a.canonical && !special;
