@@ -99,6 +99,7 @@ __device__ __forceinline__ void pick_group(double2 (&c)[MC], double2 (*sv)[MC], 
     bool used = j >= m;
     int taken = 0;
     const double thresholds[3] = {0.05, 1e-8, 0.0};
+    __syncwarp(gm);  // the caller's reads of the group's rows precede the first accepted vector's store
     for (int tp = 0; tp < 3 && taken < need; ++tp) {
         const double thr = thresholds[tp];
         int start = 0;
