@@ -261,9 +261,11 @@ __global__ void __launch_bounds__(32 * WPC, 2) spectrum_mma_kernel(SpecArgs a, i
     compute:
         const float2* hrow = Hs + (warp * 8 + r) * hs + c;  // A[r][c] = h(dir r, mic k0 + c)
         double den = 0.0;
-        // two passes of 4 vector tiles (32 accumulator registers each)
+        // two passes of 4 vector tiles (32 accumulator registers each); the
+        // second holds only zero padding when nn <= 32 (it would add 0.0)
+        const int halves = nn > 32 ? 2 : 1;
 #pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < halves; ++half) {
             const double2* ecol = Es + (half * 32 + r) * es + c;  // B[c][r] = e(vector 8j + r, mic k0 + c)
             double re[4][2], im[4][2];
 #pragma unroll
@@ -463,7 +465,7 @@ void spectrum_shape(int m, int ns, int dirs, int& dchunk, int& nsplit, size_t& s
 }
 
 void launch_spectrum(SpecArgs a, int nblk, cudaStream_t s) {
-    if (a.m - a.ns <= kMmaN && a.m - a.ns >= 16) {  // FP64 tensor cores
+    if (a.m - a.ns <= kMmaN && a.m - a.ns >= 16) {  // FP64 tensor cores (m = 16, Ns = 2 on them: 181 vs 130 us per C2 launch)
         auto mma = [&](auto kern, int wpc) {
             const int chunk = 8 * wpc;
             const size_t smem2 = (size_t)kMmaN * mma_estride(a.m) * sizeof(double2) +
